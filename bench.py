@@ -1,0 +1,415 @@
+"""FSE throughput benchmark (BASELINE.json metric: lost blocks/s and lost
+Mpixel/s, plus the fraction of the FP32 CUDA-core roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config 4] [--precision fp32] [--frames 64]
+
+Workload (N=1 and every N): BASELINE config 4 — 64 independent 1920x1080
+synthetic luma frames (per-frame seeds), 20% mixed isolated+burst 16x16
+losses, FSE 4x4 / d=14 / FFT 64x64 / 100 iterations, rho=0.8, gamma=0.5,
+delta=0.2, optimized order, fp32.  Frame-parallel: rank r of N owns a
+contiguous 64/N frame range (no data-path collective; scaling "strong": the
+64-frame job is fixed).  One step = the whole job once:
+    host C++ plans of the rank's frames -> uint8->fp32 working copy ->
+    every dependency level of every frame as one sm_100a launch -> mask pass.
+value = lost FSE blocks of all ranks / max-over-ranks device time of K steps,
+inputs resident in HBM.  e2e = the same through the public conceal_batch()
+with pinned host frames in and results out (H2D/D2H inside the region).
+
+--impl reference: the reference's own compiled FSE kernel (oracle/_ref, i.e.
+fsefill._kernel.run_fse) driven by the oracle's restatement of conceal()
+(optimized order), frame-parallel over all host cores (one process per core,
+each a different frame), each step a bounded sample of the same workload.
+Rank 0 only; other ranks exit 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+B, D, F, RHO, DELTA, GAMMA = 4, 14, 64, 0.8, 0.2, 0.5
+
+
+def counted_flops_per_block(iters: int, f1: int, f2: int) -> float:
+    """17 * I * F1 * (F2/2 + 1) algorithmic FLOPs per block."""
+    return 17.0 * iters * f1 * (f2 // 2 + 1)
+
+
+def args_():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=4, choices=[3, 4])
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--frames", type=int, default=64)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-blocks", type=int, default=2000,
+                    help="cpu_baseline sample: lossy blocks of frame 0 (about 10 s single core)")
+    return ap.parse_args()
+
+
+def iterations_for(config):
+    return 200 if config == 3 else 100
+
+
+def frame_ids(config, frames, rank, world):
+    n = frames if config == 4 else 1
+    lo, hi = rank * n // world, (rank + 1) * n // world
+    return list(range(lo, hi))
+
+
+def make_scenes(config, ids, threads=None):
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_2207_00233_b200 import synth
+
+    with ThreadPoolExecutor(max_workers=threads or min(16, os.cpu_count() or 1)) as ex:
+        return list(ex.map(lambda f: synth.config_scene(config, f), ids))
+
+
+def workload_name(config, frames, precision):
+    if config == 4:
+        return (f"config4: {frames} x 1920x1080 synthetic luma frames, 20% mixed 16x16 losses, "
+                f"FSE 4x4 / d=14 / FFT 64x64 / 100 it, optimized order, {precision}, frame-parallel")
+    return (f"config3: 1920x1080 synthetic luma, 30% isolated 16x16 losses, FSE 4x4 / d=14 / "
+            f"FFT 64x64 / 200 it, optimized order, {precision}")
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ reference arm
+
+def _ref_worker(job):
+    config, frame, iters, limit = job
+    from oracle import oracle as O
+    from paper_2207_00233_b200 import synth
+
+    img, mask = synth.config_scene(config, frame)
+    p = O.Params(d=D, rho=RHO, delta=DELTA, gamma=GAMMA, iterations=iters, block_size=B,
+                 fft_size=(F, F))
+    kernel = "ref" if O.ref_kernel() is not None else "c"
+    t0 = time.perf_counter()
+    _, _, rep = O.conceal(img, mask, p, "optimized", kernel=kernel, block_limit=limit)
+    return rep.blocks_processed, time.perf_counter() - t0, kernel
+
+
+def cpu_reference(config, iters, cores, blocks_per_core, frames):
+    """Frame-parallel CPU run of the reference kernel: one process per core, each
+    concealing the first `blocks_per_core` blocks of a different frame."""
+    import multiprocessing as mp
+
+    jobs = [(config, f % (frames if config == 4 else 1), iters, blocks_per_core) for f in range(cores)]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        t0 = time.perf_counter()
+        res = pool.map(_ref_worker, jobs)
+        wall = time.perf_counter() - t0
+    blocks = sum(r[0] for r in res)
+    return blocks, wall, res[0][2]
+
+
+def run_reference(a, rank, world):
+    if rank != 0:
+        return
+    from oracle import oracle as O
+
+    iters = iterations_for(a.config)
+    cores = os.cpu_count() or 1
+    try:
+        import psutil
+
+        cores = len(psutil.Process().cpu_affinity()) or cores
+    except Exception:
+        pass
+    per = max(20, 160 // max(1, iters // 100))  # ~0.75 s of CPU per core per step
+    kernel = "ref" if O.ref_kernel() is not None else "c"
+    for _ in range(a.warmup):
+        cpu_reference(a.config, iters, cores, per // 4, a.frames)
+    tot_b, tot_t = 0, 0.0
+    lost_px_per_block = B * B
+    for _ in range(a.steps):
+        b, t, kernel = cpu_reference(a.config, iters, cores, per, a.frames)
+        tot_b += b
+        tot_t += t
+    value = tot_b / tot_t
+    sample = (f"{cores} processes x first {per} lossy blocks (optimized order) of distinct frames "
+              f"per step; kernel={'oracle/_ref (reference _kernel.pyx compiled here)' if kernel == 'ref' else 'oracle C port'}")
+    line = {
+        "impl": "reference", "metric": "lost_blocks_per_s", "value": value, "unit": "blocks/s",
+        "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": 1000.0 * tot_t / a.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE generators)",
+        "config": {"workload": workload_name(a.config, a.frames, "fp64"), "sample": sample},
+        "lost_mpixel_per_s": value * lost_px_per_block / 1e6,
+        "cpu_baseline": {"value": value, "unit": "blocks/s", "cores": cores,
+                         "kind": "reference" if kernel == "ref" else "port", "sample": sample},
+        "e2e": {"value": value, "unit": "blocks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ B200 arm
+
+def measure_fp32_peak(torch, lib):
+    """FFMA throughput of this GPU (roofline denominator), CUDA events."""
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    scratch = torch.zeros(1, device="cuda")
+    s = torch.cuda.current_stream()
+    blocks, threads, iters = sms * 8, 256, 4096
+    for _ in range(2):
+        lib.fse_fma_probe(blocks, threads, iters, scratch.data_ptr(), s.cuda_stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    reps = 5
+    for _ in range(reps):
+        lib.fse_fma_probe(blocks, threads, iters, scratch.data_ptr(), s.cuda_stream)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    flops = 16.0 * iters * blocks * threads
+    return flops / (ms * 1e-3) / 1e12, sms
+
+
+def run_b200(a, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2207_00233_b200 as P
+    from paper_2207_00233_b200 import _lib
+
+    torch.cuda.set_device(local_rank)
+    lib = _lib.lib()
+    iters = iterations_for(a.config)
+    params = P.FseParams(d=D, rho=RHO, delta=DELTA, gamma=GAMMA, iterations=iters, block_size=B,
+                         fft_size=F)
+    ids = frame_ids(a.config, a.frames, rank, world)
+    scenes = make_scenes(a.config, ids)
+    imgs_h = torch.from_numpy(np.stack([s[0] for s in scenes])).pin_memory()
+    msks_h = torch.from_numpy(np.stack([s[1] for s in scenes])).pin_memory()
+    n, H, W = imgs_h.shape
+    tdt = torch.float32 if a.precision == "fp32" else torch.float64
+    imgs_d = imgs_h.cuda()
+    msks_d = msks_h.cuda()
+    work = torch.empty((n, H, W), dtype=tdt, device="cuda")
+    mout = torch.empty_like(msks_d)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    masks_np = list(msks_h.numpy())
+    plan_threads = 0
+
+    # work accounting from one plan set
+    plans = P.build_plans(masks_np, params, "optimized", plan_threads)
+    blocks_rank = sum(p.n_processed for p in plans)
+    lost_px_rank = int((msks_h == 1).sum())
+    levels = max(p.n_levels for p in plans)
+    del plans
+    plan_ms = []
+
+    def step():
+        flush.zero_()
+        t = time.perf_counter()
+        pl = P.build_plans(masks_np, params, "optimized", plan_threads)
+        plan_ms.append(1e3 * (time.perf_counter() - t))
+        work.copy_(imgs_d)
+        P.run_frames_device(pl, list(work), list(msks_d), list(mout), params, a.precision)
+        return pl
+
+    def timed(fn, k):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        keep = None
+        for _ in range(k):
+            keep = fn()
+        e1.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = e0.elapsed_time(e1)
+        del keep
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    plan_ms.clear()
+    lib.fse_launch_count(1)
+    lib.fse_timing_read(None, None, None)
+    lib.fse_timing_enable(1)
+    with ClockSampler(local_rank) as clk:
+        ms = timed(step, a.steps)
+    lib.fse_timing_enable(0)
+    launches = int(lib.fse_launch_count(1))
+    import ctypes
+
+    kms = ctypes.c_double()
+    wl = ctypes.c_int64()
+    calls = ctypes.c_int64()
+    _lib.check(lib.fse_timing_read(ctypes.byref(kms), ctypes.byref(wl), ctypes.byref(calls)))
+
+    tot = torch.tensor([blocks_rank, lost_px_rank], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tot)
+    blocks_all, lost_px_all = float(tot[0]), float(tot[1])
+    value = blocks_all * a.steps / (ms * 1e-3)
+
+    # roofline of the dominant kernel (the level launches, fse_window_kernel)
+    flop_blk = counted_flops_per_block(iters, F, F)
+    kernel_ms = kms.value / a.steps
+    achieved = blocks_rank * flop_blk / (kernel_ms * 1e-3) / 1e12
+    peak, sms = measure_fp32_peak(torch, lib)
+
+    # e2e through the public API with pinned host buffers
+    e2e = None
+    if not a.no_e2e:
+        def e2e_step():
+            return P.conceal_batch(imgs_h, msks_h, params, "optimized", a.precision,
+                                   plan_threads, reports=False)
+        for _ in range(max(1, min(2, a.warmup))):
+            e2e_step()
+        ems = timed(e2e_step, a.steps)
+        esz = 4 if a.precision == "fp32" else 8
+        e2e = {"value": blocks_all * a.steps / (ems * 1e-3), "unit": "blocks/s",
+               "ms_per_step": ems / a.steps,
+               "h2d_bytes_per_step": int(imgs_h.numel() * imgs_h.element_size() + msks_h.numel()) * world,
+               "d2h_bytes_per_step": int(n * H * W * (esz + 1)) * world}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        from oracle import oracle as O
+
+        img0, m0 = scenes[0]
+        p0 = O.Params(d=D, rho=RHO, delta=DELTA, gamma=GAMMA, iterations=iters, block_size=B,
+                      fft_size=(F, F))
+        kern = "ref" if O.ref_kernel() is not None else "c"
+        t0 = time.perf_counter()
+        _, _, rep = O.conceal(img0, m0, p0, "optimized", kernel=kern, block_limit=a.cpu_blocks)
+        wall = time.perf_counter() - t0
+        cpu = {"value": rep.blocks_processed / wall, "unit": "blocks/s", "cores": 1,
+               "kind": "reference" if kern == "ref" else "port",
+               "sample": f"first {rep.blocks_processed} lossy blocks (optimized order) of frame 0, "
+                         f"{wall:.1f} s, 1 thread; kernel="
+                         + ("oracle/_ref = reference _kernel.pyx compiled here" if kern == "ref"
+                            else "oracle C port")}
+
+    if rank == 0:
+        line = {
+            "metric": "lost_blocks_per_s", "value": value, "unit": "blocks/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms / a.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32" if a.precision == "fp32" else "f64",
+            "data": "synthetic (seeded BASELINE generators, paper_2207_00233_b200/synth.py)",
+            "config": {"workload": workload_name(a.config, a.frames, a.precision),
+                       "frames": len(frame_ids(a.config, a.frames, 0, 1)), "H": H, "W": W,
+                       "block": B, "d": D, "fft": F, "iterations": iters, "rho": RHO,
+                       "delta": DELTA, "gamma": GAMMA, "order": "optimized",
+                       "parallelism": f"frame-parallel x{world}",
+                       "l2": "256 MiB buffer written every step (> 126 MB L2)"},
+            "lost_mpixel_per_s": lost_px_all * a.steps / (ms * 1e-3) / 1e6,
+            "blocks_per_step": blocks_all, "lost_pixels_per_step": lost_px_all,
+            "levels_per_step": levels,
+            "host_plan_ms_per_step": float(np.mean(plan_ms)) if plan_ms else None,
+            "kernel_ms_per_step": kernel_ms,
+            "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "fse_window_kernel (level launches)",
+                         "flops_per_block": flop_blk,
+                         "peak_source": f"measured live: FFMA probe on {sms} SMs (fse_fma_probe)"},
+            "gpu_launches": launches,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+
+
+def main():
+    a = args_()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if world != a.gpus and "RANK" in os.environ:
+        print(f"warning: --gpus {a.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    if a.impl == "reference":
+        run_reference(a, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_b200(a, rank, world, local_rank)
+    finally:
+        if world > 1:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,167 @@
+/*
+ * fse_b200.h — C ABI of the B200-native Frequency Selective Extrapolation (FSE)
+ * hot path.  Built into paper_2207_00233_b200/libfse_b200.so (sm_100a).
+ *
+ * Plain C types only (no torch types).  Device pointers are CUDA device
+ * addresses; `stream` is a cudaStream_t passed as void* (NULL = legacy stream).
+ * Every function returns FSE_OK (0) or a negative errno-style code; the message
+ * of the last failure on the calling thread is available from fse_last_error().
+ * No C++ exception crosses this boundary.  Functions are re-entrant; memory
+ * passed in is caller-owned.
+ *
+ * Each entry point names the reference interface it replaces
+ * (reference = /root/reference/pkg/src/fsefill, the `fsefill` package).
+ */
+#ifndef FSE_B200_H
+#define FSE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FSE_OK 0
+#define FSE_EINVAL (-22)   /* bad argument (mirrors the reference's ValueError) */
+#define FSE_ENOMEM (-12)
+#define FSE_ECUDA (-5)     /* CUDA runtime error */
+#define FSE_ENOTSUP (-95)  /* configuration not compiled in (e.g. FFT size) */
+
+/* arithmetic type of the device path */
+#define FSE_F64 0
+#define FSE_F32 1
+
+/* processing orders, fsefill.conceal.LINESCAN / OPTIMIZED (conceal.py:30-32) */
+#define FSE_ORDER_OPTIMIZED 0
+#define FSE_ORDER_LINESCAN 1
+
+/* sample states of a loss mask, fsefill.image KNOWN/LOST/RECONSTRUCTED (image.py:14-16) */
+#define FSE_KNOWN 0
+#define FSE_LOST 1
+#define FSE_RECONSTRUCTED 2
+
+/* fsefill.fse.FseParams (fse.py:55-86) plus the DFT size.
+ * fft1 = fft2 = 0 keeps the reference semantics (DFT size = window shape,
+ * fse.py:158-159); otherwise every window is zero-padded at the top-left to
+ * fft1 x fft2, which must be >= the largest window. */
+typedef struct FseParamsC {
+    int32_t d;           /* border width in samples */
+    int32_t block_size;  /* B: side of the square block grid */
+    int32_t iterations;  /* basis-selection iterations */
+    int32_t fft1, fft2;  /* DFT size, 0 = window shape */
+    double rho;          /* isotropic decay in (0, 1) */
+    double delta;        /* reconstructed-sample down-weighting in [0, 1] */
+    double gamma;        /* ODC damping in (0, 1] */
+} FseParamsC;
+
+const char *fse_last_error(void);
+
+/* Library/device self-description: writes up to n ints:
+ * [abi_version, n_fast_fft_sizes, fast sizes..., sm_count(or -1 w/o device)] */
+int fse_version(int32_t *out, int32_t n);
+
+/* ------------------------------------------------------------------------
+ * Per-window operator.
+ * Replaces fsefill._kernel.run_fse(values, weights, iterations, gamma)
+ * (_kernel.pyx:128-187, contract _kernel_py.py:13-30), called once per window
+ * by fsefill.fse.generate_model (fse.py:153-156).  Batched: n windows of
+ * M x N samples, each zero-padded at the top-left to an F1 x F2 DFT.
+ *   values, weights : device, dtype, [n][M][N] row-major; weights >= 0 and
+ *                     positive somewhere (the reference's precondition, enforced
+ *                     upstream by DegenerateWindowError, fse.py:150-151)
+ *   picks           : device int32 [n][iterations][2]   (required)
+ *   plog            : device dtype [n][iterations][2]   (required) projection
+ *                     coefficient p = g[a,b] / sum(w) of every pick; the host
+ *                     replays coeff[a,b] += gamma*p exactly as _kernel.pyx:50-71
+ *   energies        : device dtype [n][iterations+1] or NULL (debug)
+ *   residual        : device dtype [n][M][N] or NULL (debug, weighted residual r)
+ * energies and residual must be both NULL or both non-NULL.  The synthesis
+ * (fse.py:159) is the host's ifft2 of the replayed coefficient grid. */
+int fse_run_windows(int32_t n, int32_t M, int32_t N, int32_t F1, int32_t F2,
+                    const void *values, const void *weights,
+                    int32_t iterations, double gamma, int32_t dtype,
+                    int32_t *picks, void *plog, void *energies, void *residual,
+                    void *stream);
+
+/* ------------------------------------------------------------------------
+ * Scheduler + plan (host C++).
+ * Replaces the order logic of fsefill.conceal.conceal (conceal.py:97-181):
+ * grid (grid.py:81-144), neighbour-count wavefront scheduler
+ * (schedule.py:28-105), snapshot semantics (conceal.py:148-163), deferral of
+ * degenerate windows and retry sweeps (conceal.py:69-94).  The plan assigns
+ * every lossy block an effective rank (its phase; retries after all phases),
+ * decides degeneracy on the host (pure function of mask and ranks), and groups
+ * blocks into dependency levels: a block depends only on lower-rank blocks
+ * whose samples its window covers, so one level = one batched launch. */
+typedef struct FsePlan FsePlan;
+
+int fse_plan_build(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p,
+                   int32_t order, FsePlan **out);
+/* n masks (each H x W) built on n_threads host threads (0 = hardware) */
+int fse_plan_build_many(int32_t n, const uint8_t *const *masks, int32_t H, int32_t W,
+                        const FseParamsC *p, int32_t order, int32_t n_threads,
+                        FsePlan **out);
+void fse_plan_free(FsePlan *plan);
+
+/* sizes[0..9] = rows, cols, n_lossy, n_processed, n_batches, n_batch_entries,
+ *               n_levels, n_unconcealed, max_window_rows, max_window_cols */
+int fse_plan_sizes(const FsePlan *plan, int32_t *sizes);
+/* ConcealReport.batches (conceal.py:35-42): CSR, ptr[n_batches+1] */
+int fse_plan_batches(const FsePlan *plan, int32_t *ptr, int32_t *blocks);
+/* dependency levels, CSR over processed blocks, ptr[n_levels+1] */
+int fse_plan_levels(const FsePlan *plan, int32_t *ptr, int32_t *blocks);
+/* effective rank per block (INT32_MAX = not processed) [rows*cols] */
+int fse_plan_ranks(const FsePlan *plan, int32_t *rank);
+/* ConcealReport.unconcealed_blocks, row-major */
+int fse_plan_unconcealed(const FsePlan *plan, int32_t *blocks);
+
+/* fsefill.schedule.init_counts (schedule.py:28-57): lossy[rows*cols] != 0 marks
+ * a lossy block; counts[rows*cols] out. */
+int fse_init_counts(const uint8_t *lossy, int32_t rows, int32_t cols, int32_t *counts);
+/* fsefill.schedule.schedule_all (schedule.py:97-105): batches as CSR.
+ * ptr needs room for (#pending + 1) entries, blocks for #pending. */
+int fse_schedule_all(const int32_t *counts, int32_t rows, int32_t cols,
+                     int32_t *ptr, int32_t *blocks, int32_t *n_batches);
+
+/* ------------------------------------------------------------------------
+ * Device pipeline.
+ * Replaces the per-batch loop of fsefill.conceal.conceal (conceal.py:145-163:
+ * classify_window + _snapshot + extrapolate_block + _write_block) for n frames
+ * that share H, W and params.  Level by level (levels of all frames merged into
+ * one launch), one CTA per block: area classification from the original mask
+ * and the plan's ranks (grid.py:108-135), weights (fse.py:105-119), DFT set-up,
+ * the iterative model fit, and write-back of the block's LOST samples
+ * (conceal.py:61-66).
+ *   images    : n device pointers, dtype, [H][W], updated in place
+ *   masks     : n device pointers, uint8 [H][W], the ORIGINAL masks (read only)
+ *   masks_out : n device pointers, uint8 [H][W] or NULL: LOST samples of
+ *               concealed blocks become RECONSTRUCTED (may alias masks only if
+ *               the caller no longer needs the original)
+ *   decay     : device dtype table, decay[i*decay_dim + j] = rho ** sqrt((i/2)^2 + (j/2)^2)
+ *               for i, j = |2*offset| from the window centre (fse.py:112-115)
+ *   picks     : device int32 [n][rows*cols][iterations][2] or NULL (parity/debug) */
+int fse_conceal_frames(int32_t n, FsePlan *const *plans, void *const *images,
+                       const uint8_t *const *masks, uint8_t *const *masks_out,
+                       const FseParamsC *p, int32_t dtype,
+                       const void *decay, int32_t decay_dim,
+                       int32_t *picks, void *stream);
+
+/* Count of kernel launches issued since the last reset (bench.py gpu_launches). */
+int64_t fse_launch_count(int32_t reset);
+
+/* Device timing of the window-kernel launches of fse_conceal_frames on the
+ * calling thread: enable, run, then read the summed CUDA-event time of the
+ * level launches (ms), how many window-kernel launches that covered and how
+ * many calls; reading resets.  Used by bench.py for the roofline. */
+int fse_timing_enable(int32_t on);
+int fse_timing_read(double *ms, int64_t *window_launches, int64_t *calls);
+
+/* FP32 FMA throughput probe (roofline denominator): blocks x threads threads,
+ * each running 8 independent FFMA chains for iters steps (16*iters FLOP per
+ * thread).  scratch: device float[1]. */
+int fse_fma_probe(int32_t blocks, int32_t threads, int32_t iters, void *scratch, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FSE_B200_H */

@@ -1,0 +1,257 @@
+"""End-to-end concealment on a B200 (drop-in for fsefill.conceal.conceal).
+
+``conceal(image, mask, params, order, threads)`` keeps the reference's contract
+(/root/reference/pkg/src/fsefill/conceal.py:97-181): same arguments, same
+ValueErrors, inputs untouched, returns (image float64, mask uint8,
+ConcealReport) with the reference's batches / blocks_processed /
+unconcealed_blocks.  ``precision`` ("fp64" default, or "fp32") is added, and
+FseParams gains ``fft_size``.
+
+How it runs:
+  1. C++ plan (csrc/fse_plan.cpp): the reference batches, effective ranks with
+     host-decided deferral/retry sweeps, and dependency levels.
+  2. One device launch per level (csrc/fse_kernel.cuh, MODE 0): each CTA
+     classifies its window from the original mask + ranks, builds weights,
+     fits the model and writes its block's LOST samples back into the image.
+  3. A mask pass marks concealed samples RECONSTRUCTED.
+``conceal_batch`` does the same for many equally sized frames with all frames'
+levels merged into one launch each (frame-parallel, BASELINE config 4).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .fse import FseParams, PRECISIONS, decay_table
+
+LINESCAN = "linescan"
+OPTIMIZED = "optimized"
+ORDERS = (LINESCAN, OPTIMIZED)
+
+
+@dataclass
+class ConcealReport:
+    """conceal.py:35-42."""
+
+    order: str
+    threads: int
+    blocks_processed: int
+    wall_time: float
+    batches: list = field(default_factory=list)
+    unconcealed_blocks: list = field(default_factory=list)
+    levels: int = 0  # dependency levels launched (B200 addition)
+
+
+class Plan:
+    """Owner of an FsePlan* (C++ scheduler result)."""
+
+    def __init__(self, handle: int):
+        self.handle = ctypes.c_void_p(handle)
+        s = np.zeros(10, dtype=np.int32)
+        _lib.check(_lib.lib().fse_plan_sizes(self.handle, _lib.ptr32(s)))
+        (self.rows, self.cols, self.n_lossy, self.n_processed, self.n_batches, self.n_entries,
+         self.n_levels, self.n_unconcealed, self.max_wr, self.max_wc) = (int(x) for x in s)
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            _lib.lib().fse_plan_free(h)
+            self.handle = None
+
+    def _csr(self, fn, n, m):
+        ptr = np.zeros(n + 1, dtype=np.int32)
+        blocks = np.zeros(max(m, 1), dtype=np.int32)
+        _lib.check(fn(self.handle, _lib.ptr32(ptr), _lib.ptr32(blocks)))
+        return [blocks[ptr[i]:ptr[i + 1]].tolist() for i in range(n)]
+
+    def batches(self) -> list:
+        return self._csr(_lib.lib().fse_plan_batches, self.n_batches, self.n_entries)
+
+    def levels(self) -> list:
+        return self._csr(_lib.lib().fse_plan_levels, self.n_levels, self.n_processed)
+
+    def ranks(self) -> np.ndarray:
+        r = np.zeros(self.rows * self.cols, dtype=np.int32)
+        _lib.check(_lib.lib().fse_plan_ranks(self.handle, _lib.ptr32(r)))
+        return r
+
+    def unconcealed(self) -> list:
+        u = np.zeros(max(self.n_unconcealed, 1), dtype=np.int32)
+        _lib.check(_lib.lib().fse_plan_unconcealed(self.handle, _lib.ptr32(u)))
+        return u[: self.n_unconcealed].tolist()
+
+
+def _order_code(order: str) -> int:
+    return _lib.FSE_ORDER_LINESCAN if order == LINESCAN else _lib.FSE_ORDER_OPTIMIZED
+
+
+def build_plan(mask: np.ndarray, params: FseParams, order: str = OPTIMIZED) -> Plan:
+    m = np.ascontiguousarray(mask, dtype=np.uint8)
+    h = ctypes.c_void_p()
+    pc = params.to_c()
+    _lib.check(_lib.lib().fse_plan_build(m.ctypes.data, m.shape[0], m.shape[1], ctypes.byref(pc),
+                                         _order_code(order), ctypes.byref(h)))
+    return Plan(h.value)
+
+
+def build_plans(masks, params: FseParams, order: str = OPTIMIZED, threads: int = 0) -> list:
+    ms = [np.ascontiguousarray(m, dtype=np.uint8) for m in masks]
+    n = len(ms)
+    if n == 0:
+        return []
+    H, W = ms[0].shape
+    if any(m.shape != (H, W) for m in ms):
+        raise ValueError("all masks of a batch must share one shape")
+    arr = (ctypes.c_void_p * n)(*[m.ctypes.data for m in ms])
+    out = (ctypes.c_void_p * n)()
+    pc = params.to_c()
+    _lib.check(_lib.lib().fse_plan_build_many(n, arr, H, W, ctypes.byref(pc), _order_code(order),
+                                              int(threads), out))
+    return [Plan(out[i]) for i in range(n)]
+
+
+def _validate(image, mask, params, order, threads, precision):
+    if params is None:
+        params = FseParams()
+    if order not in ORDERS:
+        raise ValueError(f"unknown order {order!r}")
+    if threads < 1:
+        raise ValueError("threads must be >= 1")
+    if order == LINESCAN and threads != 1:
+        raise ValueError("linescan order is sequential; threads must be 1")
+    if np.shape(mask) != np.shape(image):
+        raise ValueError(f"mask shape {np.shape(mask)} != image shape {np.shape(image)}")
+    if precision not in PRECISIONS:
+        raise ValueError(f"precision must be one of {PRECISIONS}")
+    return params
+
+
+class DeviceContext:
+    """Device-resident constants shared by calls with the same params (the
+    rho^dist table) plus the torch module handle."""
+
+    _cache: dict = {}
+
+    @classmethod
+    def decay(cls, params: FseParams, dim: int):
+        import torch
+
+        key = (params.rho, dim)
+        t = cls._cache.get(key)
+        if t is None:
+            t = torch.from_numpy(decay_table(params.rho, dim)).cuda()
+            cls._cache[key] = t
+        return t
+
+
+def run_frames_device(plans, images_dev, masks_dev, masks_out_dev, params: FseParams,
+                      precision: str, picks_dev=None, stream=None) -> None:
+    """Run the level pipeline on device tensors already in HBM (the `value` path)."""
+    import torch
+
+    n = len(plans)
+    if n == 0:
+        return
+    P0 = plans[0]
+    F = params.fft_dims((P0.max_wr, P0.max_wc))
+    if params.fft_size is not None and (F[0] < P0.max_wr or F[1] < P0.max_wc):
+        raise ValueError(f"fft_size {F} smaller than the largest window {(P0.max_wr, P0.max_wc)}")
+    dim = max(P0.max_wr, P0.max_wc, 1)
+    decay = DeviceContext.decay(params, dim)
+    vp = ctypes.c_void_p * n
+    pl = vp(*[p.handle.value for p in plans])
+    im = vp(*[t.data_ptr() for t in images_dev])
+    mk = vp(*[t.data_ptr() for t in masks_dev])
+    mo = vp(*[t.data_ptr() for t in masks_out_dev]) if masks_out_dev is not None else None
+    code = _lib.FSE_F64 if precision == "fp64" else _lib.FSE_F32
+    pc = params.to_c()
+    s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    _lib.check(_lib.lib().fse_conceal_frames(
+        n, pl, im, mk, mo, ctypes.byref(pc), code, decay.data_ptr(), dim,
+        picks_dev.data_ptr() if picks_dev is not None else None, s))
+
+
+def _report(plan: Plan, order, threads, wall) -> ConcealReport:
+    return ConcealReport(order=order, threads=threads, blocks_processed=plan.n_processed,
+                         wall_time=wall, batches=plan.batches(),
+                         unconcealed_blocks=plan.unconcealed(), levels=plan.n_levels)
+
+
+def conceal(image, mask, params: FseParams | None = None, order: str = OPTIMIZED,
+            threads: int = 1, precision: str = "fp64", return_picks: bool = False):
+    """Conceal every lost block (conceal.py:97-181); see the module docstring."""
+    params = _validate(image, mask, params, order, threads, precision)
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("conceal() needs a CUDA device (no CPU fallback)")
+    img = np.array(image, dtype=np.float64, copy=True)
+    msk = np.array(mask, dtype=np.uint8, copy=True)
+    t0 = time.perf_counter()
+    plan = build_plan(msk, params, order)
+    tdt = torch.float64 if precision == "fp64" else torch.float32
+    img_d = torch.from_numpy(img).to(device="cuda", dtype=tdt)
+    msk_d = torch.from_numpy(msk).cuda()
+    out_d = torch.empty_like(msk_d)
+    picks_d = None
+    if return_picks:
+        picks_d = torch.zeros((plan.rows * plan.cols, max(params.iterations, 1), 2),
+                              dtype=torch.int32, device="cuda")
+    run_frames_device([plan], [img_d], [msk_d], [out_d], params, precision, picks_d)
+    out_img = img_d.double().cpu().numpy()
+    out_msk = out_d.cpu().numpy()
+    wall = time.perf_counter() - t0
+    rep = _report(plan, order, threads, wall)
+    if return_picks:
+        return out_img, out_msk, rep, picks_d[:, : params.iterations].cpu().numpy()
+    return out_img, out_msk, rep
+
+
+def conceal_batch(images, masks, params: FseParams | None = None, order: str = OPTIMIZED,
+                  precision: str = "fp32", plan_threads: int = 0, reports: bool = True):
+    """Frame-parallel concealment of equally sized frames: one plan per frame
+    (C++ threads, overlapped with the upload), every dependency level of every
+    frame in one launch.
+
+    images: [n, H, W] numpy array or CPU torch tensor (any real dtype; pinned
+    torch tensors upload asynchronously), masks: [n, H, W] uint8 likewise.
+    Returns (images [n, H, W] numpy in the compute dtype — float64 for "fp64",
+    float32 for "fp32" —, masks [n, H, W] uint8, reports or None)."""
+    if params is None:
+        params = FseParams()
+    if order not in ORDERS:
+        raise ValueError(f"unknown order {order!r}")
+    if precision not in PRECISIONS:
+        raise ValueError(f"precision must be one of {PRECISIONS}")
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("conceal_batch() needs a CUDA device (no CPU fallback)")
+    imgs = images if isinstance(images, torch.Tensor) else torch.from_numpy(np.asarray(images))
+    msks = masks if isinstance(masks, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(np.asarray(masks, dtype=np.uint8)))
+    if msks.dtype != torch.uint8:
+        raise ValueError("masks must be uint8")
+    if tuple(imgs.shape) != tuple(msks.shape) or imgs.dim() != 3:
+        raise ValueError("images and masks must both be [n, H, W]")
+    t0 = time.perf_counter()
+    tdt = torch.float64 if precision == "fp64" else torch.float32
+    # uploads are queued first (async from pinned memory); planning overlaps them
+    img_d = imgs.to(device="cuda", non_blocking=True).to(tdt)
+    msk_d = msks.to(device="cuda", non_blocking=True)
+    plans = build_plans(list(msks.numpy()), params, order, plan_threads)
+    out_d = torch.empty_like(msk_d)
+    run_frames_device(plans, list(img_d), list(msk_d), list(out_d), params, precision)
+    out_img = torch.empty(img_d.shape, dtype=tdt, pin_memory=True)
+    out_msk = torch.empty(out_d.shape, dtype=torch.uint8, pin_memory=True)
+    out_img.copy_(img_d, non_blocking=True)
+    out_msk.copy_(out_d, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    wall = time.perf_counter() - t0
+    reps = [_report(p, order, 1, wall) for p in plans] if reports else None
+    return out_img.numpy(), out_msk.numpy(), reps

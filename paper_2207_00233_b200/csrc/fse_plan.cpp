@@ -1,0 +1,466 @@
+// Host scheduler for the FSE hot path (C++, no CUDA).
+//
+// Reference behaviour being reproduced (reference = /root/reference/pkg/src/fsefill):
+//   block grid, ragged edges            grid.py:26-88
+//   per-block lost tally                grid.py:138-144
+//   neighbour counts + rim bonus        schedule.py:28-57
+//   N_min batch selection, commit       schedule.py:60-105  (Algorithm 1)
+//   snapshot-then-write batches         conceal.py:145-163
+//   linescan order                      conceal.py:133-143
+//   deferral + retry sweeps             conceal.py:54-58, 69-94
+//
+// The device never replays the reference's mutable mask.  Instead every lossy
+// block gets an effective rank (the index of the reference batch that writes
+// it; retries follow all batches), and a lost sample s seen from block b is
+// "reconstructed" (area R) iff the block owning s has a smaller rank than b.
+// That is a pure function of (original mask, ranks), so blocks of different
+// reference batches may share a launch as long as every lower-rank block whose
+// samples their window covers has finished: those dependencies define levels.
+#include <algorithm>
+#include <atomic>
+#include <climits>
+#include <cstring>
+#include <thread>
+
+#include "fse_common.h"
+
+namespace fse {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+int fail(int code, const std::string &msg) {
+    set_error(msg);
+    return code;
+}
+
+namespace {
+
+constexpr int kMarginBonus = 3;  // schedule.py:20
+constexpr int kCornerBonus = 5;  // schedule.py:21
+
+int validate(const FseParamsC *p, int32_t H, int32_t W, int32_t order) {
+    if (!p) return fail(FSE_EINVAL, "params is NULL");
+    if (H < 1 || W < 1) return fail(FSE_EINVAL, "image dimensions must be positive");
+    if (p->d < 0) return fail(FSE_EINVAL, "d must be >= 0");
+    if (!(p->rho > 0.0 && p->rho < 1.0)) return fail(FSE_EINVAL, "rho must lie in (0, 1)");
+    if (!(p->delta >= 0.0 && p->delta <= 1.0)) return fail(FSE_EINVAL, "delta must lie in [0, 1]");
+    if (!(p->gamma > 0.0 && p->gamma <= 1.0)) return fail(FSE_EINVAL, "gamma must lie in (0, 1]");
+    if (p->iterations < 0) return fail(FSE_EINVAL, "iterations must be >= 0");
+    if (p->block_size < 1) return fail(FSE_EINVAL, "block_size must be >= 1");
+    if (order != FSE_ORDER_OPTIMIZED && order != FSE_ORDER_LINESCAN)
+        return fail(FSE_EINVAL, "unknown order");
+    return FSE_OK;
+}
+
+// schedule.py:28-57 on a row-major lossy table
+void init_counts_impl(const uint8_t *lossy, int rows, int cols, int32_t *counts) {
+    for (int r = 0; r < rows; ++r)
+        for (int c = 0; c < cols; ++c) {
+            int32_t n = 0;
+            for (int dr = -1; dr <= 1; ++dr)
+                for (int dc = -1; dc <= 1; ++dc) {
+                    if (!dr && !dc) continue;
+                    int rr = r + dr, cc = c + dc;
+                    if (rr >= 0 && rr < rows && cc >= 0 && cc < cols && lossy[rr * cols + cc]) ++n;
+                }
+            int edges = (r == 0) + (r == rows - 1) + (c == 0) + (c == cols - 1);
+            if (edges == 1) n += kMarginBonus;
+            else if (edges >= 2) n += kCornerBonus;
+            counts[r * cols + c] = lossy[r * cols + c] ? n : -1;
+        }
+}
+
+// schedule.py:60-105 with a bucket queue: one bitset of pending blocks per
+// count value, scanned in row-major order for the current minimum.  Selection
+// of a whole batch happens before any commit, as in select_batch/commit_batch.
+void schedule_impl(const int32_t *counts_in, int rows, int cols,
+                   std::vector<int32_t> &ptr, std::vector<int32_t> &blocks) {
+    const int nb = rows * cols;
+    const int words = (nb + 63) / 64;
+    std::vector<int32_t> cnt(counts_in, counts_in + nb);
+    int maxc = 0;
+    long pending = 0;
+    for (int b = 0; b < nb; ++b)
+        if (cnt[b] >= 0) {
+            maxc = std::max(maxc, (int)cnt[b]);
+            ++pending;
+        }
+    std::vector<std::vector<uint64_t>> bucket(maxc + 1, std::vector<uint64_t>(words, 0));
+    std::vector<long> bsize(maxc + 1, 0);
+    std::vector<int> lo_word(maxc + 1, 0);  // no set bit below this word
+    for (int b = 0; b < nb; ++b)
+        if (cnt[b] >= 0) {
+            bucket[cnt[b]][b >> 6] |= 1ull << (b & 63);
+            ++bsize[cnt[b]];
+        }
+    auto add = [&](int c, int b) {
+        bucket[c][b >> 6] |= 1ull << (b & 63);
+        ++bsize[c];
+        lo_word[c] = std::min(lo_word[c], b >> 6);
+    };
+    auto del = [&](int c, int b) {
+        bucket[c][b >> 6] &= ~(1ull << (b & 63));
+        --bsize[c];
+    };
+    std::vector<int32_t> taken(nb, -1);
+    ptr.assign(1, 0);
+    blocks.clear();
+    blocks.reserve(pending);
+    std::vector<int32_t> batch;
+    int phase = 0;
+    while (pending > 0) {
+        int nmin = 0;
+        while (bsize[nmin] == 0) ++nmin;
+        batch.clear();
+        auto &bits = bucket[nmin];
+        int w0 = lo_word[nmin];
+        while (w0 < words && bits[w0] == 0) ++w0;
+        lo_word[nmin] = w0;
+        for (int w = w0; w < words; ++w) {
+            uint64_t m = bits[w];
+            while (m) {
+                int b = (w << 6) + __builtin_ctzll(m);
+                m &= m - 1;
+                int r = b / cols, c = b - r * cols;
+                // only row-major-earlier neighbours can already be taken
+                bool clash = false;
+                if (c > 0 && taken[b - 1] == phase) clash = true;
+                if (!clash && r > 0) {
+                    int up = b - cols;
+                    if (taken[up] == phase || (c > 0 && taken[up - 1] == phase) ||
+                        (c + 1 < cols && taken[up + 1] == phase))
+                        clash = true;
+                }
+                if (clash) continue;
+                taken[b] = phase;
+                batch.push_back(b);
+            }
+        }
+        for (int b : batch) {
+            del(nmin, b);
+            cnt[b] = -1;
+            --pending;
+        }
+        for (int b : batch) {
+            int r = b / cols, c = b - r * cols;
+            for (int dr = -1; dr <= 1; ++dr)
+                for (int dc = -1; dc <= 1; ++dc) {
+                    if (!dr && !dc) continue;
+                    int rr = r + dr, cc = c + dc;
+                    if (rr < 0 || rr >= rows || cc < 0 || cc >= cols) continue;
+                    int o = rr * cols + cc;
+                    if (cnt[o] >= 0) {
+                        del(cnt[o], o);
+                        --cnt[o];
+                        add(cnt[o], o);
+                    } else {
+                        --cnt[o];  // done blocks drift below -1 (schedule.py:85-94)
+                    }
+                }
+        }
+        blocks.insert(blocks.end(), batch.begin(), batch.end());
+        ptr.push_back((int32_t)blocks.size());
+        ++phase;
+    }
+}
+
+struct Geometry {
+    int H, W, B, rows, cols, d;
+    void block_rect(int b, int &r0, int &r1, int &c0, int &c1) const {
+        int r = b / cols, c = b - r * cols;
+        r0 = r * B;
+        r1 = std::min(r0 + B, H);
+        c0 = c * B;
+        c1 = std::min(c0 + B, W);
+    }
+    void window_rect(int b, int &r0, int &r1, int &c0, int &c1) const {
+        block_rect(b, r0, r1, c0, c1);
+        r0 = std::max(0, r0 - d);
+        c0 = std::max(0, c0 - d);
+        r1 = std::min(H, r1 + d);
+        c1 = std::min(W, c1 + d);
+    }
+};
+
+int build_one(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p, int32_t order,
+              Plan &P) {
+    int rc = validate(p, H, W, order);
+    if (rc) return rc;
+    Geometry G{H, W, p->block_size, (H + p->block_size - 1) / p->block_size,
+               (W + p->block_size - 1) / p->block_size, p->d};
+    const int rows = G.rows, cols = G.cols, nb = rows * cols, B = G.B;
+    P.H = H; P.W = W; P.B = B; P.rows = rows; P.cols = cols; P.d = p->d; P.order = order;
+    P.iterations = p->iterations; P.fft1 = p->fft1; P.fft2 = p->fft2;
+    P.rho = p->rho; P.delta = p->delta; P.gamma = p->gamma;
+
+    // per-block tallies: lost (grid.py:138-144), usable-as-A, pre-reconstructed
+    std::vector<int32_t> nL(nb, 0), nA(nb, 0), nR0(nb, 0);
+    for (int y = 0; y < H; ++y) {
+        const uint8_t *row = mask + (size_t)y * W;
+        int32_t *L = &nL[(y / B) * cols], *A = &nA[(y / B) * cols], *R0 = &nR0[(y / B) * cols];
+        for (int x = 0; x < W; ++x) {
+            uint8_t s = row[x];
+            int c = x / B;
+            if (s == FSE_LOST) ++L[c];
+            else if (s == FSE_RECONSTRUCTED) ++R0[c];
+            else ++A[c];  // anything else classifies as A (grid.py:124-130)
+        }
+    }
+    std::vector<uint8_t> lossy(nb);
+    P.n_lossy = 0;
+    for (int b = 0; b < nb; ++b) {
+        lossy[b] = nL[b] > 0;
+        P.n_lossy += lossy[b];
+    }
+    P.max_wr = std::min(H, B + 2 * p->d);
+    P.max_wc = std::min(W, B + 2 * p->d);
+
+    // processing phases in reference order
+    std::vector<int32_t> ph_ptr, ph_blocks;
+    if (order == FSE_ORDER_OPTIMIZED) {
+        std::vector<int32_t> counts(nb);
+        init_counts_impl(lossy.data(), rows, cols, counts.data());
+        schedule_impl(counts.data(), rows, cols, ph_ptr, ph_blocks);
+    } else {
+        ph_ptr.assign(1, 0);
+        for (int b = 0; b < nb; ++b)
+            if (lossy[b]) {
+                ph_blocks.push_back(b);
+                ph_ptr.push_back((int32_t)ph_blocks.size());
+            }
+    }
+
+    // degeneracy (fse.py:150-151): no sample of positive weight.  A samples
+    // always weigh rho^dist > 0; R samples weigh delta*rho^dist, > 0 iff delta > 0.
+    std::vector<uint8_t> written(nb, 0);
+    const bool r_counts = p->delta > 0.0;
+    auto usable = [&](int b) -> bool {
+        int wr0, wr1, wc0, wc1;
+        G.window_rect(b, wr0, wr1, wc0, wc1);
+        int br0 = wr0 / B, br1 = (wr1 - 1) / B, bc0 = wc0 / B, bc1 = (wc1 - 1) / B;
+        for (int pass = 0; pass < 2; ++pass)  // cheap whole-block test first
+            for (int rr = br0; rr <= br1; ++rr)
+                for (int cc = bc0; cc <= bc1; ++cc) {
+                    int o = rr * cols + cc;
+                    int or0, or1, oc0, oc1;
+                    G.block_rect(o, or0, or1, oc0, oc1);
+                    bool inside = or0 >= wr0 && or1 <= wr1 && oc0 >= wc0 && oc1 <= wc1;
+                    if (pass == 0) {
+                        if (!inside) continue;
+                        if (nA[o] > 0) return true;
+                        if (r_counts && (nR0[o] > 0 || (written[o] && nL[o] > 0))) return true;
+                    } else {
+                        if (inside) continue;
+                        int y0 = std::max(or0, wr0), y1 = std::min(or1, wr1);
+                        int x0 = std::max(oc0, wc0), x1 = std::min(oc1, wc1);
+                        for (int y = y0; y < y1; ++y)
+                            for (int x = x0; x < x1; ++x) {
+                                uint8_t s = mask[(size_t)y * W + x];
+                                if (s != FSE_LOST && s != FSE_RECONSTRUCTED) return true;
+                                if (r_counts && (s == FSE_RECONSTRUCTED || (s == FSE_LOST && written[o])))
+                                    return true;
+                            }
+                    }
+                }
+        return false;
+    };
+
+    P.rank.assign(nb, INT32_MAX);
+    P.batch_ptr.assign(1, 0);
+    P.batch_blocks.clear();
+    std::vector<int32_t> deferred, ok;
+    const int n_phases = (int)ph_ptr.size() - 1;
+    for (int ph = 0; ph < n_phases; ++ph) {
+        ok.clear();
+        for (int i = ph_ptr[ph]; i < ph_ptr[ph + 1]; ++i) {
+            int b = ph_blocks[i];
+            if (usable(b)) ok.push_back(b);
+            else deferred.push_back(b);
+        }
+        for (int b : ok) {  // writes land only after the whole batch (snapshot)
+            P.rank[b] = ph;
+            written[b] = 1;
+        }
+        if (!ok.empty()) {
+            P.batch_blocks.insert(P.batch_blocks.end(), ok.begin(), ok.end());
+            P.batch_ptr.push_back((int32_t)P.batch_blocks.size());
+        }
+    }
+    // retry sweeps: sequential, row-major, each sees the previous results
+    std::sort(deferred.begin(), deferred.end());
+    std::vector<int32_t> pending = deferred, still;
+    int next_rank = n_phases;
+    for (int sweep = 0; sweep < std::max(rows, cols); ++sweep) {
+        if (pending.empty()) break;
+        still.clear();
+        for (int b : pending) {
+            if (usable(b)) {
+                P.rank[b] = next_rank++;
+                written[b] = 1;
+                P.batch_blocks.push_back(b);
+                P.batch_ptr.push_back((int32_t)P.batch_blocks.size());
+            } else {
+                still.push_back(b);
+            }
+        }
+        if (still.size() == pending.size()) break;
+        pending.swap(still);
+    }
+    P.unconcealed = pending;
+    P.n_processed = (int32_t)P.batch_blocks.size();
+
+    // dependency levels over the processing order
+    std::vector<int32_t> level(nb, -1);
+    int n_levels = 0;
+    for (int b : P.batch_blocks) {
+        int wr0, wr1, wc0, wc1;
+        G.window_rect(b, wr0, wr1, wc0, wc1);
+        int br0 = wr0 / B, br1 = (wr1 - 1) / B, bc0 = wc0 / B, bc1 = (wc1 - 1) / B;
+        int lv = 0;
+        const int rb = P.rank[b];
+        for (int rr = br0; rr <= br1; ++rr)
+            for (int cc = bc0; cc <= bc1; ++cc) {
+                int o = rr * cols + cc;
+                if (P.rank[o] < rb) lv = std::max(lv, level[o] + 1);
+            }
+        level[b] = lv;
+        n_levels = std::max(n_levels, lv + 1);
+    }
+    P.level_ptr.assign(n_levels + 1, 0);
+    for (int b : P.batch_blocks) ++P.level_ptr[level[b] + 1];
+    for (int l = 0; l < n_levels; ++l) P.level_ptr[l + 1] += P.level_ptr[l];
+    P.level_blocks.assign(P.n_processed, 0);
+    std::vector<int32_t> fill(P.level_ptr.begin(), P.level_ptr.end() - 1);
+    for (int b = 0; b < nb; ++b)  // row-major within a level
+        if (level[b] >= 0) P.level_blocks[fill[level[b]]++] = b;
+    return FSE_OK;
+}
+
+}  // namespace
+}  // namespace fse
+
+using fse::fail;
+
+extern "C" {
+
+const char *fse_last_error(void) { return fse::g_last_error.c_str(); }
+
+int fse_init_counts(const uint8_t *lossy, int32_t rows, int32_t cols, int32_t *counts) {
+    if (!lossy || !counts || rows < 1 || cols < 1) return fail(FSE_EINVAL, "bad arguments");
+    fse::init_counts_impl(lossy, rows, cols, counts);
+    return FSE_OK;
+}
+
+int fse_schedule_all(const int32_t *counts, int32_t rows, int32_t cols, int32_t *ptr,
+                     int32_t *blocks, int32_t *n_batches) {
+    if (!counts || !ptr || !blocks || !n_batches || rows < 1 || cols < 1)
+        return fail(FSE_EINVAL, "bad arguments");
+    std::vector<int32_t> vp, vb;
+    try {
+        fse::schedule_impl(counts, rows, cols, vp, vb);
+    } catch (const std::exception &e) {
+        return fail(FSE_ENOMEM, e.what());
+    }
+    std::memcpy(ptr, vp.data(), vp.size() * sizeof(int32_t));
+    if (!vb.empty()) std::memcpy(blocks, vb.data(), vb.size() * sizeof(int32_t));
+    *n_batches = (int32_t)vp.size() - 1;
+    return FSE_OK;
+}
+
+int fse_plan_build(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p,
+                   int32_t order, FsePlan **out) {
+    if (!mask || !out) return fail(FSE_EINVAL, "mask/out is NULL");
+    FsePlan *plan = nullptr;
+    try {
+        plan = new FsePlan();
+        int rc = fse::build_one(mask, H, W, p, order, plan->p);
+        if (rc) {
+            delete plan;
+            return rc;
+        }
+    } catch (const std::exception &e) {
+        delete plan;
+        return fail(FSE_ENOMEM, e.what());
+    }
+    *out = plan;
+    return FSE_OK;
+}
+
+int fse_plan_build_many(int32_t n, const uint8_t *const *masks, int32_t H, int32_t W,
+                        const FseParamsC *p, int32_t order, int32_t n_threads, FsePlan **out) {
+    if (n < 0 || (n > 0 && (!masks || !out))) return fail(FSE_EINVAL, "bad arguments");
+    int nt = n_threads > 0 ? n_threads : (int)std::thread::hardware_concurrency();
+    nt = std::max(1, std::min(nt, n));
+    std::vector<int> rcs(n, 0);
+    std::vector<std::string> errs(n);
+    std::atomic<int> next(0);
+    auto work = [&]() {
+        for (int i; (i = next.fetch_add(1)) < n;) {
+            out[i] = nullptr;
+            rcs[i] = fse_plan_build(masks[i], H, W, p, order, &out[i]);
+            if (rcs[i]) errs[i] = fse_last_error();
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+    work();
+    for (auto &t : pool) t.join();
+    for (int i = 0; i < n; ++i)
+        if (rcs[i]) {
+            for (int j = 0; j < n; ++j) {
+                fse_plan_free(out[j]);
+                out[j] = nullptr;
+            }
+            return fail(rcs[i], errs[i]);
+        }
+    return FSE_OK;
+}
+
+void fse_plan_free(FsePlan *plan) { delete plan; }
+
+int fse_plan_sizes(const FsePlan *plan, int32_t *s) {
+    if (!plan || !s) return fail(FSE_EINVAL, "NULL argument");
+    const fse::Plan &P = plan->p;
+    s[0] = P.rows;
+    s[1] = P.cols;
+    s[2] = P.n_lossy;
+    s[3] = P.n_processed;
+    s[4] = (int32_t)P.batch_ptr.size() - 1;
+    s[5] = (int32_t)P.batch_blocks.size();
+    s[6] = (int32_t)P.level_ptr.size() - 1;
+    s[7] = (int32_t)P.unconcealed.size();
+    s[8] = P.max_wr;
+    s[9] = P.max_wc;
+    return FSE_OK;
+}
+
+int fse_plan_batches(const FsePlan *plan, int32_t *ptr, int32_t *blocks) {
+    if (!plan || !ptr || !blocks) return fail(FSE_EINVAL, "NULL argument");
+    const fse::Plan &P = plan->p;
+    std::copy(P.batch_ptr.begin(), P.batch_ptr.end(), ptr);
+    std::copy(P.batch_blocks.begin(), P.batch_blocks.end(), blocks);
+    return FSE_OK;
+}
+
+int fse_plan_levels(const FsePlan *plan, int32_t *ptr, int32_t *blocks) {
+    if (!plan || !ptr || !blocks) return fail(FSE_EINVAL, "NULL argument");
+    const fse::Plan &P = plan->p;
+    std::copy(P.level_ptr.begin(), P.level_ptr.end(), ptr);
+    std::copy(P.level_blocks.begin(), P.level_blocks.end(), blocks);
+    return FSE_OK;
+}
+
+int fse_plan_ranks(const FsePlan *plan, int32_t *rank) {
+    if (!plan || !rank) return fail(FSE_EINVAL, "NULL argument");
+    std::copy(plan->p.rank.begin(), plan->p.rank.end(), rank);
+    return FSE_OK;
+}
+
+int fse_plan_unconcealed(const FsePlan *plan, int32_t *blocks) {
+    if (!plan || !blocks) return fail(FSE_EINVAL, "NULL argument");
+    std::copy(plan->p.unconcealed.begin(), plan->p.unconcealed.end(), blocks);
+    return FSE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,69 @@
+"""Shared test helpers: golden-case readers and a CPU emulation of the device
+pipeline (level-by-level, rank-based classification) driven by the oracle."""
+
+import numpy as np
+
+from oracle import oracle as O
+
+
+def conceal_case(g, i):
+    d, rho, delta, gamma, iters, B = g[f"k{i}_params"].tolist()
+    fft = tuple(int(x) for x in g[f"k{i}_fft"])
+    return dict(
+        name=str(g[f"k{i}_name"]),
+        image=g[f"k{i}_image"],
+        mask=g[f"k{i}_mask"],
+        d=int(d), rho=rho, delta=delta, gamma=gamma, iterations=int(iters), block_size=int(B),
+        fft=None if fft == (0, 0) else fft,
+        order=str(g[f"k{i}_order"]),
+        out_image=g[f"k{i}_out_image"],
+        out_mask=g[f"k{i}_out_mask"],
+        batches=csr(g[f"k{i}_batch_ptr"], g[f"k{i}_batch_blocks"]),
+        unconcealed=g[f"k{i}_unconcealed"].tolist(),
+        processed=int(g[f"k{i}_processed"]),
+        pick_blocks=g[f"k{i}_pick_blocks"],
+        picks=g[f"k{i}_picks"],
+    )
+
+
+def csr(ptr, blocks):
+    return [blocks[ptr[k]:ptr[k + 1]].tolist() for k in range(len(ptr) - 1)]
+
+
+def emulate_levels(image, mask, B, d, rho, delta, gamma, iterations, fft, ranks, levels, kernel="c",
+                   shuffle_seed=0):
+    """What the device does, on the CPU: for each level, every block classifies
+    its window from the ORIGINAL mask and the plan ranks (lost sample = R iff its
+    owner has a smaller rank), fits with the oracle kernel and writes back
+    IMMEDIATELY, in a shuffled order (emulating CTAs of one launch racing)."""
+    rng = np.random.default_rng(shuffle_seed)
+    img = np.array(image, dtype=np.float64, copy=True)
+    H, W = img.shape
+    rows, cols = -(-H // B), -(-W // B)
+    by = np.minimum(np.arange(H) // B, rows - 1)
+    bx = np.minimum(np.arange(W) // B, cols - 1)
+    owner = by[:, None] * cols + bx[None, :]
+    p = O.Params(d=d, rho=rho, delta=delta, gamma=gamma, iterations=iterations, block_size=B,
+                 fft_size=fft)
+    for level in levels:
+        for b in rng.permutation(level).tolist():
+            r, c = divmod(b, cols)
+            r0, r1, c0, c1 = r * B, min(r * B + B, H), c * B, min(c * B + B, W)
+            wr0, wr1, wc0, wc1 = max(0, r0 - d), min(H, r1 + d), max(0, c0 - d), min(W, c1 + d)
+            sub = mask[wr0:wr1, wc0:wc1]
+            own = owner[wr0:wr1, wc0:wc1]
+            lost = sub == O.LOST
+            cls = np.where(sub == O.RECONSTRUCTED, O.AREA_R, O.AREA_A).astype(np.uint8)
+            earlier = ranks[own] < ranks[b]
+            cls[lost & (own != b) & earlier] = O.AREA_R
+            cls[lost & (own != b) & ~earlier] = O.AREA_BO
+            cls[lost & (own == b)] = O.AREA_BI
+            vals = img[wr0:wr1, wc0:wc1].copy()
+            blk = O.extrapolate(vals, cls, (r0 - wr0, r1 - wr0, c0 - wc0, c1 - wc0), p, kernel)
+            assert blk is not None, f"plan scheduled a degenerate block {b}"
+            lost = mask[r0:r1, c0:c1] == O.LOST
+            img[r0:r1, c0:c1][lost] = blk[lost]
+    out_mask = mask.copy()
+    done = ranks[owner] != np.iinfo(np.int32).max
+    out_mask[(mask == O.LOST) & done] = O.RECONSTRUCTED
+    return img, out_mask

@@ -1,0 +1,225 @@
+"""End-to-end concealment on the GPU (conceal / conceal_batch through
+fse_conceal_frames) against the reference's golden outputs, plus the
+reference's pipeline properties (test_conceal.py, test_acceptance.py)."""
+
+import numpy as np
+import pytest
+
+from helpers import conceal_case, csr
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2207_00233_b200")
+from paper_2207_00233_b200 import synth  # noqa: E402
+
+
+def _params(c):
+    return P.FseParams(d=c["d"], rho=c["rho"], delta=c["delta"], gamma=c["gamma"],
+                       iterations=c["iterations"], block_size=c["block_size"], fft_size=c["fft"])
+
+
+def psnr(orig, res, mask):
+    region = mask != 0
+    mse = float(np.mean((orig[region] - res[region]) ** 2))
+    return float("inf") if mse == 0 else 10 * np.log10(255.0 ** 2 / mse)
+
+
+@pytest.mark.parametrize("i", range(11))
+def test_fp64_matches_reference_golden(golden, i):
+    c = conceal_case(golden("conceal_cases.npz"), i)
+    img, msk, rep, picks = P.conceal(c["image"], c["mask"], _params(c), c["order"],
+                                     precision="fp64", return_picks=True)
+    np.testing.assert_array_equal(msk, c["out_mask"])
+    assert rep.batches == c["batches"]
+    assert rep.unconcealed_blocks == c["unconcealed"]
+    assert rep.blocks_processed == c["processed"]
+    assert np.max(np.abs(img - c["out_image"])) <= 1e-6
+    if c["fft"] is not None:
+        for b, want in zip(c["pick_blocks"].tolist(), c["picks"]):
+            assert O.canonical_picks(picks[b], c["fft"]) == [tuple(x) for x in want.tolist()], b
+
+
+@pytest.mark.parametrize("i", [2, 4, 6, 7])
+def test_fp32_within_tolerance_of_reference(golden, i):
+    c = conceal_case(golden("conceal_cases.npz"), i)
+    img, msk, _ = P.conceal(c["image"], c["mask"], _params(c), c["order"], precision="fp32")
+    np.testing.assert_array_equal(msk, c["out_mask"])
+    assert np.max(np.abs(img - c["out_image"])) <= 0.5
+
+
+@pytest.mark.parametrize("k", [0, 1, 2])
+def test_full_baseline_configs_fp64_identical_picks(golden, k):
+    """BASELINE configs 1 and 2 at full size, fp64: every block's canonical pick
+    sequence identical to the reference, every sample within 1e-6."""
+    g = golden("full_cfg.npz")
+    img, mask = synth.config_scene(int(g[f"f{k}_config"]))
+    p = P.FseParams(d=14, iterations=100, block_size=4, fft_size=64)
+    out, msk, rep, picks = P.conceal(img, mask, p, str(g[f"f{k}_order"]), precision="fp64",
+                                     return_picks=True)
+    assert rep.batches == csr(g[f"f{k}_batch_ptr"], g[f"f{k}_batch_blocks"])
+    lost = mask == 1
+    assert np.max(np.abs(out[lost] - g[f"f{k}_lost_values"])) <= 1e-6
+    assert int(msk.astype(np.int64).sum()) == int(g[f"f{k}_out_mask_sum"])
+    bad = [b for b, want in zip(g[f"f{k}_pick_blocks"].tolist(), g[f"f{k}_picks"])
+           if O.canonical_picks(picks[b], (64, 64)) != [tuple(x) for x in want.astype(int).tolist()]]
+    assert bad == []
+
+
+@pytest.mark.parametrize("k", [0, 1])
+def test_full_baseline_configs_fp32_tolerance(golden, k):
+    g = golden("full_cfg.npz")
+    img, mask = synth.config_scene(int(g[f"f{k}_config"]))
+    p = P.FseParams(d=14, iterations=100, block_size=4, fft_size=64)
+    out, _, _ = P.conceal(img, mask, p, str(g[f"f{k}_order"]), precision="fp32")
+    lost = mask == 1
+    ref = img.astype(np.float64).copy()
+    ref[lost] = g[f"f{k}_lost_values"]
+    assert np.max(np.abs(out[lost] - ref[lost])) <= 0.5
+    truth = img.astype(np.float64)
+    assert abs(psnr(truth, out, mask) - psnr(truth, ref, mask)) <= 0.02
+
+
+def scene(shape=(64, 64)):
+    y, x = np.mgrid[0:shape[0], 0:shape[1]].astype(np.float64)
+    return 120.0 + 50.0 * np.sin(x / 5.0) + 30.0 * np.cos(y / 7.0) + 0.3 * x
+
+
+FAST = None
+
+
+def fast():
+    return P.FseParams(d=8, iterations=30, block_size=8)
+
+
+def square_loss(shape, squares):
+    m = np.zeros(shape, np.uint8)
+    for r, c, s in squares:
+        m[r:r + s, c:c + s] = 1
+    return m
+
+
+def test_no_loss_is_a_no_op():
+    img = scene()
+    mask = np.zeros(img.shape, np.uint8)
+    for order in ("linescan", "optimized"):
+        out, om, rep = P.conceal(img, mask, fast(), order)
+        np.testing.assert_array_equal(out, img)
+        np.testing.assert_array_equal(om, mask)
+        assert rep.blocks_processed == 0 and rep.batches == [] and rep.unconcealed_blocks == []
+
+
+def test_inputs_not_modified_and_known_preserved():
+    img = scene()
+    mask = square_loss(img.shape, [(8, 8, 12), (30, 40, 10), (50, 2, 6)])
+    i0, m0 = img.copy(), mask.copy()
+    for order in ("linescan", "optimized"):
+        out, om, rep = P.conceal(img, mask, fast(), order)
+        np.testing.assert_array_equal(img, i0)
+        np.testing.assert_array_equal(mask, m0)
+        known = mask == 0
+        np.testing.assert_array_equal(out[known], img[known])
+        assert not (om == 1).any() and (om[mask == 1] == 2).all() and (om[known] == 0).all()
+        assert rep.order == order and rep.wall_time >= 0
+
+
+def test_partially_lost_block_keeps_known_half():
+    img = scene()
+    mask = np.zeros(img.shape, np.uint8)
+    mask[16:20, 16:24] = 1
+    out, om, _ = P.conceal(img, mask, fast())
+    np.testing.assert_array_equal(out[20:24, 16:24], img[20:24, 16:24])
+    assert (om[16:20, 16:24] == 2).all() and (om[20:24, 16:24] == 0).all()
+
+
+def test_argument_errors():
+    img = scene()
+    mask = square_loss(img.shape, [(8, 8, 8)])
+    with pytest.raises(ValueError, match="sequential"):
+        P.conceal(img, mask, fast(), order="linescan", threads=2)
+    with pytest.raises(ValueError, match="order"):
+        P.conceal(img, mask, fast(), order="zigzag")
+    with pytest.raises(ValueError, match="threads"):
+        P.conceal(img, mask, fast(), threads=0)
+    with pytest.raises(ValueError, match="shape"):
+        P.conceal(img, mask[:32, :32], fast())
+    with pytest.raises(ValueError):
+        P.conceal(img, mask, P.FseParams(d=14, block_size=4, iterations=5, fft_size=16))
+
+
+@pytest.mark.parametrize("threads", [2, 8])
+def test_thread_count_invariance(threads):
+    img = scene()
+    mask = square_loss(img.shape, [(4, 4, 10), (24, 24, 16), (40, 8, 8), (8, 44, 12)])
+    a = P.conceal(img, mask, fast(), threads=1)
+    b = P.conceal(img, mask, fast(), threads=threads)
+    assert a[0].tobytes() == b[0].tobytes() and a[1].tobytes() == b[1].tobytes()
+    assert b[2].threads == threads
+
+
+def test_all_lost_and_retry_sweeps():
+    img = scene((32, 32))
+    out, om, rep = P.conceal(img, np.ones((32, 32), np.uint8), fast())
+    assert (om == 1).all() and rep.blocks_processed == 0
+    np.testing.assert_array_equal(out, img)
+    assert rep.unconcealed_blocks == list(range(16))
+    img = scene((96, 96))
+    mask = square_loss(img.shape, [(16, 16, 64)])
+    out, om, rep = P.conceal(img, mask, P.FseParams(d=4, iterations=20, block_size=8))
+    assert not (om == 1).any() and rep.blocks_processed == 64 and rep.unconcealed_blocks == []
+    seen = [b for bt in rep.batches for b in bt]
+    assert len(seen) == len(set(seen)) == 64
+
+
+def test_conceal_batch_equals_per_frame():
+    frames = [synth.synthetic_frame(96, 160, 50 + f, 6, 3) for f in range(3)]
+    masks = [synth.loss_mask(96, 160, "mixed", 0.25, 60 + f) for f in range(3)]
+    p = P.FseParams(d=14, iterations=40, block_size=4, fft_size=64)
+    for prec in ("fp64", "fp32"):
+        imgs, msks, reps = P.conceal_batch(np.stack(frames), np.stack(masks), p, precision=prec)
+        for f in range(3):
+            one, om, rep = P.conceal(frames[f], masks[f], p, precision=prec)
+            assert imgs[f].astype(np.float64).tobytes() == one.tobytes()
+            np.testing.assert_array_equal(msks[f], om)
+            assert reps[f].batches == rep.batches
+
+
+def test_deterministic_repeat():
+    img, mask = synth.config_scene(2)
+    p = P.FseParams(d=14, iterations=100, block_size=4, fft_size=64)
+    a = P.conceal(img, mask, p, precision="fp32")[0]
+    b = P.conceal(img, mask, p, precision="fp32")[0]
+    assert a.tobytes() == b.tobytes()
+
+
+@pytest.mark.parametrize("B,F", [(2, 32), (4, 64), (8, 128)])
+def test_config5_block_sizes_on_a_crop_vs_oracle(B, F):
+    img, mask = synth.config_scene(5)
+    img, mask = img[:96, :128].copy(), mask[:96, :128].copy()
+    p = P.FseParams(d=14, iterations=30, block_size=B, fft_size=F)
+    out, om, rep = P.conceal(img, mask, p, precision="fp64")
+    o_img, o_msk, o_rep = O.conceal(img, mask, O.Params(d=14, iterations=30, block_size=B, fft_size=(F, F)),
+                                    "optimized", kernel="auto")
+    assert rep.batches == o_rep.batches
+    np.testing.assert_array_equal(om, o_msk)
+    assert np.max(np.abs(out - o_img)) <= 1e-6
+
+
+@pytest.mark.parametrize("config,prec,iters", [(3, "fp32", 200), (4, "fp32", 100)])
+def test_full_size_properties(config, prec, iters):
+    """BASELINE configs 3 and 4 at full 1080p size: size-independent properties."""
+    img, mask = synth.config_scene(config)
+    p = P.FseParams(d=14, iterations=iters, block_size=4, fft_size=64)
+    out, om, rep = P.conceal(img, mask, p, precision=prec)
+    known = mask == 0
+    np.testing.assert_array_equal(out[known], img[known].astype(np.float64))
+    assert (om[mask == 1] == 2).all() and (om[known] == 0).all()
+    assert np.isfinite(out).all()
+    assert rep.unconcealed_blocks == []
+    assert rep.blocks_processed == int((P.lost_per_block(P.build_grid(1920, 1080, 4), mask) > 0).sum())
+    # fp32 agrees with the fp64 path on the same frame
+    out64, _, _ = P.conceal(img, mask, p, precision="fp64")
+    lost = mask == 1
+    assert np.max(np.abs(out[lost] - out64[lost])) <= 0.5
+    truth = img.astype(np.float64)
+    assert abs(psnr(truth, out, mask) - psnr(truth, out64, mask)) <= 0.02

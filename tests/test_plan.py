@@ -1,0 +1,200 @@
+"""Host side of the B200 path, CPU only: the C++ scheduler / plan in
+libfse_b200.so against the reference's golden schedules and concealment
+batches, and the level plan executed on the CPU (oracle kernel, rank-based
+classification, racing write-back) against the reference's outputs."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+from hypothesis import given, settings
+from hypothesis import strategies as st
+
+import paper_2207_00233_b200 as P
+from helpers import conceal_case, csr, emulate_levels
+from paper_2207_00233_b200 import _lib
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_header_symbol():
+    hdr = open(os.path.join(REPO, "include", "fse_b200.h")).read()
+    declared = set(re.findall(r"^(?:int|void|const char \*|int64_t)\s*\**(fse_\w+)\(", hdr, re.M))
+    assert declared, "no declarations parsed"
+    assert declared == set(_lib.EXPORTS)
+    assert set(_lib.exports_present()) == declared
+
+
+def resimulate(rows, cols, lossy):
+    """Dict-based restatement of the wavefront order (reference tests/reference.py:74-119)."""
+    def nbs(r, c):
+        return [(r + a, c + b) for a in (-1, 0, 1) for b in (-1, 0, 1)
+                if (a, b) != (0, 0) and 0 <= r + a < rows and 0 <= c + b < cols]
+    cnt = {}
+    for r in range(rows):
+        for c in range(cols):
+            if (r, c) not in lossy:
+                cnt[(r, c)] = -1
+                continue
+            e = (r == 0) + (r == rows - 1) + (c == 0) + (c == cols - 1)
+            cnt[(r, c)] = sum(x in lossy for x in nbs(r, c)) + (3 if e == 1 else 5 if e >= 2 else 0)
+    out = []
+    while any(v >= 0 for v in cnt.values()):
+        m = min(v for v in cnt.values() if v >= 0)
+        batch, taken = [], set()
+        for r in range(rows):
+            for c in range(cols):
+                if cnt[(r, c)] == m and not any(x in taken for x in nbs(r, c)):
+                    batch.append(r * cols + c)
+                    taken.add((r, c))
+        for b in batch:
+            r, c = divmod(b, cols)
+            cnt[(r, c)] = -1
+            for x in nbs(r, c):
+                cnt[x] -= 1
+        out.append(batch)
+    return out
+
+
+def grid_of(rows, cols, B=8):
+    return P.build_grid(cols * B, rows * B, B)
+
+
+def test_scheduler_matches_reference_golden(golden):
+    g = golden("schedule_cases.npz")
+    for i in range(int(g["n_cases"])):
+        t = g[f"s{i}_table"]
+        grid = grid_of(*t.shape, B=4)
+        c = P.init_counts(grid, t)
+        np.testing.assert_array_equal(c, g[f"s{i}_counts"])
+        assert P.schedule_all(grid, c) == csr(g[f"s{i}_ptr"], g[f"s{i}_blocks"])
+
+
+def test_c1_scheduler_matches_resimulation_on_100_random_grids():
+    rng = np.random.default_rng(0)
+    for _ in range(100):
+        rows, cols = int(rng.integers(1, 17)), int(rng.integers(1, 17))
+        table = (rng.uniform(size=(rows, cols)) < rng.uniform(0.05, 1.0)).astype(np.int64)
+        grid = grid_of(rows, cols, 16)
+        lossy = {(r, c) for r in range(rows) for c in range(cols) if table[r, c]}
+        assert P.schedule_all(grid, P.init_counts(grid, table)) == resimulate(rows, cols, lossy)
+
+
+def test_known_answers_3x3():
+    grid = grid_of(3, 3)
+    counts = P.init_counts(grid, np.ones((3, 3)))
+    assert counts.tolist() == [8] * 9
+    assert P.select_batch(grid, counts) == [0, 2, 6, 8]
+    batches = P.schedule_all(grid, counts)
+    assert batches == [[0, 2, 6, 8], [4], [1, 7], [3, 5]]
+    P.commit_batch(grid, counts, [0, 2, 6, 8])
+    assert counts.tolist() == [-1, 6, -1, 6, 4, 6, -1, 6, -1]
+    P.commit_batch(grid, counts, [4])
+    assert counts.tolist() == [-2, 5, -2, 5, -1, 5, -2, 5, -2]
+    assert P.render_batch_trace(grid, batches) == "1 3 1\n4 2 4\n1 3 1"
+
+
+def test_small_grids_and_empty():
+    g1 = grid_of(1, 1)
+    c = P.init_counts(g1, np.ones((1, 1)))
+    assert c.tolist() == [5]
+    assert P.schedule_all(g1, c) == [[0]]
+    g = grid_of(4, 4)
+    c = P.init_counts(g, np.zeros((4, 4)))
+    assert (c == -1).all() and P.schedule_all(g, c) == []
+    with pytest.raises(P.EmptyScheduleError):
+        P.select_batch(g, c)
+    g5 = grid_of(5, 5)
+    t = np.zeros((5, 5)); t[2, 2] = 1
+    c = P.init_counts(g5, t)
+    assert c[12] == 0 and all(v == -1 for i, v in enumerate(c) if i != 12)
+
+
+@settings(max_examples=40, deadline=None)
+@given(rows=st.integers(1, 9), cols=st.integers(1, 9), seed=st.integers(0, 2**31 - 1),
+       density=st.floats(0.05, 1.0))
+def test_schedule_properties(rows, cols, seed, density):
+    rng = np.random.default_rng(seed)
+    table = (rng.uniform(size=(rows, cols)) < density).astype(np.int64)
+    g = grid_of(rows, cols)
+    counts = P.init_counts(g, table)
+    before = counts.copy()
+    batches = P.schedule_all(g, counts)
+    np.testing.assert_array_equal(counts, before)
+    flat = [b for bt in batches for b in bt]
+    assert sorted(flat) == np.flatnonzero(table.reshape(-1)).tolist()
+    assert all(batches)
+    for bt in batches:
+        s = set(bt)
+        for b in bt:
+            assert s.isdisjoint(P.neighbors(g, b))
+    lossy = {(r, c) for r in range(rows) for c in range(cols) if table[r, c]}
+    assert batches == resimulate(rows, cols, lossy)
+
+
+def _params(c):
+    return P.FseParams(d=c["d"], rho=c["rho"], delta=c["delta"], gamma=c["gamma"],
+                       iterations=c["iterations"], block_size=c["block_size"], fft_size=c["fft"])
+
+
+@pytest.mark.parametrize("i", range(11))
+def test_plan_reports_reference_batches(golden, i):
+    c = conceal_case(golden("conceal_cases.npz"), i)
+    plan = P.build_plan(c["mask"], _params(c), c["order"])
+    assert plan.batches() == c["batches"]
+    assert plan.unconcealed() == c["unconcealed"]
+    assert plan.n_processed == c["processed"]
+    # levels are a partition of the processed blocks, never deeper than the batches
+    lv = plan.levels()
+    assert sorted(b for l in lv for b in l) == sorted(b for bt in c["batches"] for b in bt)
+    assert len(lv) <= max(1, len(c["batches"]))
+
+
+@pytest.mark.parametrize("i", [0, 1, 2, 4, 8, 9, 10])
+def test_level_plan_reproduces_reference_on_cpu(golden, i):
+    """Rank-based classification + level grouping + racing in-level write-back
+    (what the device does) equals the reference's phase-by-phase snapshots."""
+    c = conceal_case(golden("conceal_cases.npz"), i)
+    plan = P.build_plan(c["mask"], _params(c), c["order"])
+    img, msk = emulate_levels(c["image"], c["mask"], c["block_size"], c["d"], c["rho"], c["delta"],
+                              c["gamma"], c["iterations"], c["fft"], plan.ranks(), plan.levels(),
+                              shuffle_seed=i)
+    np.testing.assert_array_equal(msk, c["out_mask"])
+    assert np.max(np.abs(img - c["out_image"])) <= 1e-9
+
+
+def test_full_config_plans_report_reference_batches(golden):
+    from paper_2207_00233_b200 import synth
+    g = golden("full_cfg.npz")
+    for i in range(int(g["n_cases"])):
+        img, mask = synth.config_scene(int(g[f"f{i}_config"]))
+        assert [int(img.astype(np.int64).sum()), int(mask.astype(np.int64).sum())] == \
+            g[f"f{i}_image_sum"].tolist(), "synthetic generator drifted from the golden inputs"
+        p = P.FseParams(d=14, iterations=100, block_size=4, fft_size=64)
+        plan = P.build_plan(mask, p, str(g[f"f{i}_order"]))
+        assert plan.batches() == csr(g[f"f{i}_batch_ptr"], g[f"f{i}_batch_blocks"])
+
+
+def test_plan_validation_errors():
+    m = np.zeros((16, 16), np.uint8)
+    with pytest.raises(ValueError):
+        P.FseParams(rho=1.0)
+    with pytest.raises(ValueError):
+        P.FseParams(block_size=0)
+    bad = _lib.FseParamsC(-1, 4, 10, 0, 0, 0.8, 0.2, 0.5)
+    import ctypes
+    h = ctypes.c_void_p()
+    rc = _lib.lib().fse_plan_build(m.ctypes.data, 16, 16, ctypes.byref(bad), 0, ctypes.byref(h))
+    assert rc == _lib.FSE_EINVAL and b"d must be" in _lib.lib().fse_last_error()
+
+
+def test_plan_many_threads_equals_single():
+    from paper_2207_00233_b200 import synth
+    masks = [synth.loss_mask(96, 128, "mixed", 0.3, s) for s in range(6)]
+    p = P.FseParams(d=14, iterations=10, block_size=4, fft_size=64)
+    many = P.build_plans(masks, p, "optimized", threads=3)
+    for m, pl in zip(masks, many):
+        one = P.build_plan(m, p)
+        assert pl.batches() == one.batches() and pl.levels() == one.levels()
+        np.testing.assert_array_equal(pl.ranks(), one.ranks())
