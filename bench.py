@@ -298,11 +298,13 @@ def run_b200(a, rank, world, local_rank):
     plan_ms.clear()
     lib.fse_launch_count(1)
     lib.fse_timing_read(None, None, None)
+    lib.fse_guard_redo_count(1)
     lib.fse_timing_enable(1)
     with ClockSampler(local_rank) as clk:
         ms = timed(step, a.steps)
     lib.fse_timing_enable(0)
     launches = int(lib.fse_launch_count(1))
+    redo = int(lib.fse_guard_redo_count(1))
     import ctypes
 
     kms = ctypes.c_double()
@@ -373,6 +375,7 @@ def run_b200(a, rank, world, local_rank):
             "levels_per_step": levels,
             "host_plan_ms_per_step": float(np.mean(plan_ms)) if plan_ms else None,
             "kernel_ms_per_step": kernel_ms,
+            "fp32_guard_fp64_redo_per_step": redo / a.steps,
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": None,
                          "kernel": "fse_window_kernel (level launches)",

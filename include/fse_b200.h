@@ -146,6 +146,14 @@ int fse_conceal_frames(int32_t n, FsePlan *const *plans, void *const *images,
                        const void *decay, int32_t decay_dim,
                        int32_t *picks, void *stream);
 
+/* fp32 near-tie guard of the fast path (F = 32/64): a window whose runner-up
+ * energy comes within (tau0 + tau1 * iteration) of the maximum is recomputed
+ * by the fp64 kernel before the next level.  tau0 < 0 disables the guard.
+ * Defaults 2e-5, 3e-6.  Process-wide. */
+int fse_set_guard(double tau0, double tau1);
+/* Windows redone in fp64 by the guard, summed over timed calls (fse_timing_*). */
+int64_t fse_guard_redo_count(int32_t reset);
+
 /* Count of kernel launches issued since the last reset (bench.py gpu_launches). */
 int64_t fse_launch_count(int32_t reset);
 

@@ -24,7 +24,7 @@ LIB = os.path.join(PKG, "libfse_b200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
               "--expt-relaxed-constexpr"]
-HEADERS = ["fse_fit.cuh", "fse_common.h", "fse_kernel.cuh"]
+HEADERS = ["fse_fit.cuh", "fse_common.h", "fse_kernel.cuh", "fse_fast.cuh"]
 
 
 def _nvcc() -> str:

@@ -8,7 +8,7 @@
 #include <string>
 #include <vector>
 
-#include "fse_kernel.cuh"
+#include "fse_fast.cuh"
 
 namespace fse {
 
@@ -20,8 +20,15 @@ struct TimingState {
     bool on = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
     long long window_launches = 0;
+    // per-call guard counters copied back asynchronously (pinned), summed on read
+    std::vector<std::pair<int *, int>> redo;
 };
 static thread_local TimingState g_timing;
+
+// fp32 near-tie guard thresholds (fse_fast.cuh): redo in fp64 when
+// e1 - e2 <= (tau0 + tau1 * it) * e1.  Negative tau0 disables the guard.
+static double g_tau0 = 2e-5, g_tau1 = 3e-6;
+static long long g_redo_total = 0;
 
 // FP32 FMA throughput probe: 8 independent FFMA chains per thread.
 __global__ void fma_probe_kernel(float *out, int iters, float a, float b) {
@@ -109,6 +116,12 @@ int fse_timing_read(double *ms, int64_t *window_launches, int64_t *calls) {
         tot += t;
     }
     fse::g_timing.ev.clear();
+    cudaDeviceSynchronize();
+    for (auto &r : fse::g_timing.redo) {
+        for (int i = 0; i < r.second; ++i) fse::g_redo_total += r.first[i];
+        cudaFreeHost(r.first);
+    }
+    fse::g_timing.redo.clear();
     if (ms) *ms = tot;
     if (window_launches) *window_launches = fse::g_timing.window_launches;
     if (calls) *calls = n;
@@ -123,6 +136,18 @@ int fse_fma_probe(int32_t blocks, int32_t threads, int32_t iters, void *scratch,
     cudaError_t ce = cudaGetLastError();
     if (ce != cudaSuccess) return fail(FSE_ECUDA, cudaGetErrorString(ce));
     return FSE_OK;
+}
+
+int fse_set_guard(double tau0, double tau1) {
+    fse::g_tau0 = tau0;
+    fse::g_tau1 = tau1;
+    return FSE_OK;
+}
+
+int64_t fse_guard_redo_count(int32_t reset) {
+    const long long v = fse::g_redo_total;
+    if (reset) fse::g_redo_total = 0;
+    return v;
 }
 
 int64_t fse_launch_count(int32_t reset) {
@@ -156,6 +181,18 @@ int fse_run_windows(int32_t n, int32_t M, int32_t N, int32_t F1, int32_t F2, con
     a.picks = picks;
     cudaStream_t s = (cudaStream_t)stream;
     const bool dbg = energies != nullptr;
+    if (!dbg && F1 == F2 && fse::fast_supported(F1, M, N, 0)) {
+        fse::FastArgs f{};
+        f.values = values;
+        f.weights = weights;
+        f.plog = plog;
+        f.M = M;
+        f.N = N;
+        f.iterations = iterations;
+        f.gamma = gamma;
+        f.picks = picks;
+        return fse::fast_windows(dtype, F1, f, n, s);
+    }
     if (dtype == FSE_F64)
         return dbg ? fse::dispatch<double, 1, true>(a, n, M, N, F1, F2, 0, s)
                    : fse::dispatch<double, 1, false>(a, n, M, N, F1, F2, 0, s);
@@ -201,10 +238,12 @@ int fse_conceal_frames(int32_t n, FsePlan *const *plans, void *const *images,
         }
     }
     lvl_off[n_levels] = (int)n_entries;
-    // one staging buffer: frame table | ranks | entries
+    // one staging buffer: frame table | ranks | entries | redo list | redo counters
     const size_t off_rank = ((sizeof(fse::FrameDesc) * n + 255) / 256) * 256;
     const size_t off_ent = off_rank + ((sizeof(int32_t) * (size_t)nb * n + 255) / 256) * 256;
-    const size_t bytes = off_ent + sizeof(int2) * std::max<size_t>(n_entries, 1);
+    const size_t off_redo = off_ent + ((sizeof(int2) * std::max<size_t>(n_entries, 1) + 255) / 256) * 256;
+    const size_t off_cnt = off_redo + ((sizeof(int2) * std::max<size_t>(n_entries, 1) + 255) / 256) * 256;
+    const size_t bytes = off_cnt + sizeof(int) * std::max(n_levels, 1);
     std::vector<unsigned char> host(bytes);
     cudaStream_t s = (cudaStream_t)stream;
     unsigned char *dev = nullptr;
@@ -259,13 +298,56 @@ int fse_conceal_frames(int32_t n, FsePlan *const *plans, void *const *images,
         }
         cudaEventRecord(ev0, s);
     }
+    const bool fast = F1 == F2 && fse::fast_supported(F1, Mmax, Nmax, model_n);
+    const bool guard = fast && dtype == FSE_F32 && fse::g_tau0 >= 0.0;
+    fse::FastArgs f{};
+    if (fast) {
+        f.frames = a.frames;
+        f.H = a.H;
+        f.W = a.W;
+        f.B = a.B;
+        f.d = a.d;
+        f.rows = a.rows;
+        f.cols = a.cols;
+        f.delta = a.delta;
+        f.decay = a.decay;
+        f.decay_dim = a.decay_dim;
+        f.iterations = a.iterations;
+        f.gamma = a.gamma;
+        f.picks = a.picks;
+        f.tau0 = (float)fse::g_tau0;
+        f.tau1 = (float)fse::g_tau1;
+    }
+    int2 *redo = reinterpret_cast<int2 *>(dev + off_redo);
+    int *counters = reinterpret_cast<int *>(dev + off_cnt);
     for (int l = 0; l < n_levels && rc == FSE_OK; ++l) {
-        a.entries = reinterpret_cast<const int2 *>(dev + off_ent) + lvl_off[l];
+        const int2 *lvl = reinterpret_cast<const int2 *>(dev + off_ent) + lvl_off[l];
         const int cnt = lvl_off[l + 1] - lvl_off[l];
         if (cnt == 0) continue;
-        rc = dtype == FSE_F64 ? fse::dispatch<double, 0, false>(a, cnt, Mmax, Nmax, F1, F2, model_n, s)
-                              : fse::dispatch<float, 0, false>(a, cnt, Mmax, Nmax, F1, F2, model_n, s);
+        if (fast) {
+            f.entries = lvl;
+            f.redo_list = redo + lvl_off[l];
+            f.redo_count = counters + l;
+            rc = fse::fast_level(dtype, F1, guard, f, cnt, Mmax, Nmax, model_n, s);
+            if (rc == FSE_OK && guard) {
+                fse::FastArgs r = f;
+                r.entries = redo + lvl_off[l];
+                r.count = counters + l;
+                rc = fse::fast_redo(F1, r, cnt, Mmax, Nmax, model_n, s);
+            }
+        } else {
+            a.entries = lvl;
+            rc = dtype == FSE_F64 ? fse::dispatch<double, 0, false>(a, cnt, Mmax, Nmax, F1, F2, model_n, s)
+                                  : fse::dispatch<float, 0, false>(a, cnt, Mmax, Nmax, F1, F2, model_n, s);
+        }
         if (fse::g_timing.on) ++fse::g_timing.window_launches;
+    }
+    if (fse::g_timing.on && guard && n_levels > 0) {
+        int *hc = nullptr;
+        if (cudaMallocHost((void **)&hc, sizeof(int) * n_levels) == cudaSuccess) {
+            cudaMemcpyAsync(hc, counters, sizeof(int) * n_levels, cudaMemcpyDeviceToHost, s);
+            fse::g_timing.redo.emplace_back(hc, n_levels);
+        }
     }
     if (fse::g_timing.on) {
         cudaEventRecord(ev1, s);

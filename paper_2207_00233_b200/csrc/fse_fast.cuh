@@ -1,0 +1,526 @@
+// Fast-path FSE window kernel for square power-of-two DFT sizes F = 32 / 64
+// (BASELINE's "FFT 32x32 / 64x64"), sm_100a.  One CTA owns one window.
+//
+// Reference algorithm: fsefill._kernel.run_fse / _iterate
+// (/root/reference/pkg/src/fsefill/_kernel.pyx:14-187), see fse_fit.cuh.
+//
+// What differs from the generic kernel (fse_kernel.cuh), all for the
+// iteration loop's instruction count:
+//   * Canonical half spectrum.  Only one bin of every conjugate pair is kept:
+//     rows 1..F/2-1 whole, rows 0 and F/2 for v <= F/2.  That is exactly the
+//     set of canonical picks (reference tests/reference.py:59-71), and a pick
+//     and its twin produce the same update and coefficients, so nothing is
+//     lost; ties resolve to the smallest row-major index as in the reference's
+//     strict-'>' scan (_kernel.pyx:32-44).
+//   * Row-extended weight spectrum.  W is stored for rows -F/2 .. F (3F/2+1
+//     rows, W[r] = W[r mod F]); since picks have a <= F/2 and owned rows
+//     u <= F/2, both shifted rows u-a and u+a fall inside without a modulo,
+//     and a warp's successive rows are a compile-time stride apart, so each
+//     gather is one LDS.64/LDS.128 with an immediate offset.
+//   * Self-conjugate picks reuse the general update with p halved and made
+//     real: (p/2)(W[k-j] + W[k+j]) with W[k-j] = W[k+j]; x2 and /2 are exact.
+//   * fp32 near-tie guard.  fp32 rounding moves |g|^2 by up to ~1e-4 of the
+//     current maximum after 100 iterations, which can swap two candidates the
+//     fp64 reference separates by less than that.  Every iteration the CTA
+//     reduces the top-2 energies; when the runner-up is within tau of the
+//     winner the window is handed to the fp64 kernel (redo list) and the CTA
+//     stops.  The fp64 redo runs before the next level, so results are those
+//     of the fp64 path for every guarded window.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fse_kernel.cuh"
+
+namespace fse {
+
+template <typename T_, int F_, int NW_>
+struct FastCfg {
+    using T = T_;
+    using T2 = typename V2<T_>::type;
+    static constexpr int F = F_;
+    static constexpr int NW = NW_;
+    static constexpr int NT = NW_ * 32;
+    static constexpr int R1 = F_ / 2 + 1;       // half-plane rows
+    static constexpr int SEG = F_ / 32;         // 32-column segments per row
+    static constexpr int NSEGS = R1 * SEG;      // row segments of the half plane
+    static constexpr int NB = (NSEGS + NW_ - 1) / NW_;  // segments (bins) per thread
+    static constexpr int RSTEP = NW_ / SEG;     // row stride between a warp's segments
+    static constexpr int EXT_ROWS = 3 * F_ / 2 + 1;
+    static_assert(F_ == 32 || F_ == 64, "fast path: F = 32 or 64");
+    static_assert(NW_ % SEG == 0, "NW must be a multiple of F/32");
+    static_assert(NB <= 32, "5-bit bin tag");
+};
+
+struct FastSlot {
+    unsigned long long key;  // fp64: exact key; fp32: (energy key << 32) | ~lin
+    unsigned int second;     // fp32: energy key of the warp's runner-up
+    unsigned int pad;
+    double pre, pim;         // p = g / sum(w) of the warp's best bin
+};
+
+struct FastLayout {
+    size_t tw, slots, red, model, big, yx, yw, xs, ws, total;
+};
+
+template <typename T>
+__host__ __device__ inline FastLayout fast_layout(int F, int NW, int Mmax, int Nmax, int model_n) {
+    FastLayout L;
+    const size_t c2 = 2 * sizeof(T);
+    size_t o = 0;
+    L.tw = o; o += (size_t)F * c2;
+    o = (o + 15) & ~size_t(15);
+    L.slots = o; o += 2 * (size_t)NW * sizeof(FastSlot);
+    L.red = o; o += (size_t)(NW + 2) * sizeof(double);
+    L.model = o; o += (size_t)(model_n > 0 ? model_n : 1) * sizeof(T);
+    o = (o + 127) & ~size_t(127);
+    L.big = o;
+    const size_t R1 = F / 2 + 1;
+    const size_t HS = (size_t)(F / 2) * F * c2;       // ext row F/2 = W row 0
+    const size_t HE = (size_t)(F + 1) * F * c2;       // end of ext row F = W row F/2
+    const size_t EXT = (size_t)(3 * F / 2 + 1) * F * c2;
+    const size_t yb = (R1 * Nmax * c2 + 15) & ~size_t(15);
+    const size_t xb = ((size_t)Mmax * Nmax * sizeof(T) + 15) & ~size_t(15);
+    // Yx / Yw / xs / ws must not overlap the W half-plane rows written by the
+    // fused row pass; everything is dead once the extension rows are filled.
+    if (yb <= HS) {
+        L.yx = 0;
+        L.yw = HE;
+    } else {
+        L.yx = HE;
+        L.yw = HE + yb;
+    }
+    L.xs = L.yw + yb;
+    L.ws = L.xs + xb;
+    size_t bigb = L.ws + xb;
+    if (bigb < EXT) bigb = EXT;
+    L.total = L.big + bigb;
+    return L;
+}
+
+// Arguments of the fast kernel.
+struct FastArgs {
+    // MODE 0: pipeline level
+    const FrameDesc *frames;
+    const int2 *entries;
+    int H, W, B, d, rows, cols;
+    double delta;
+    const double *decay;
+    int decay_dim;
+    // MODE 1: window operator
+    const void *values, *weights;
+    void *plog;
+    int M, N;
+    // both
+    int iterations;
+    double gamma;
+    int32_t *picks;
+    // fp32 near-tie guard (MODE 0): redo list for the fp64 kernel
+    int2 *redo_list;
+    int *redo_count;
+    float tau0, tau1;  // guard when e1 - e2 <= (tau0 + tau1 * it) * e1
+    // persistent (redo) launch: entries[0 .. *count)
+    const int *count;
+};
+
+__device__ __forceinline__ unsigned warp_max_u32(unsigned v) { return __reduce_max_sync(0xffffffffu, v); }
+
+template <class C, int MODE, bool GUARD, typename IT>
+__device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout &L, const int entry_idx,
+                                            unsigned char *sm) {
+    using T = typename C::T;
+    using T2 = typename C::T2;
+    constexpr int F = C::F, NW = C::NW, NT = C::NT, NB = C::NB, R1 = C::R1, SEG = C::SEG;
+    constexpr int RSTEP = C::RSTEP;
+    constexpr bool IS_F32 = sizeof(T) == 4;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+
+    T2 *tw = reinterpret_cast<T2 *>(sm + L.tw);
+    FastSlot *slots = reinterpret_cast<FastSlot *>(sm + L.slots);
+    double *red = reinterpret_cast<double *>(sm + L.red);
+    unsigned char *big = sm + L.big;
+    T2 *Wext = reinterpret_cast<T2 *>(big);
+    T2 *Yx = reinterpret_cast<T2 *>(big + L.yx);
+    T2 *Yw = reinterpret_cast<T2 *>(big + L.yw);
+    T *xs = reinterpret_cast<T *>(big + L.xs);
+    T *ws = reinterpret_cast<T *>(big + L.ws);
+
+    // ---- window geometry (grid.py:108-135)
+    int M, N, br0 = 0, bc0 = 0, bh = 0, bw = 0, wr0 = 0, wc0 = 0, frame = 0, blk = 0;
+    const FrameDesc *fd = nullptr;
+    int2 entry = make_int2(0, 0);
+    if constexpr (MODE == 0) {
+        entry = A.entries[entry_idx];
+        frame = entry.x;
+        blk = entry.y;
+        fd = A.frames + frame;
+        const int r = blk / A.cols, c = blk - r * A.cols;
+        const int r0 = r * A.B, c0 = c * A.B;
+        const int r1 = min(r0 + A.B, A.H), c1 = min(c0 + A.B, A.W);
+        wr0 = max(0, r0 - A.d);
+        wc0 = max(0, c0 - A.d);
+        M = min(A.H, r1 + A.d) - wr0;
+        N = min(A.W, c1 + A.d) - wc0;
+        br0 = r0 - wr0;
+        bc0 = c0 - wc0;
+        bh = r1 - r0;
+        bw = c1 - c0;
+    } else {
+        M = A.M;
+        N = A.N;
+    }
+
+    // ---- e^{+j 2 pi k / F}
+    for (int k = t; k < F; k += NT) {
+        double s, c;
+        sincospi(2.0 * k / F, &s, &c);
+        tw[k] = T2{(T)c, (T)s};
+    }
+
+    // ---- staging: classes -> weights (fse.py:105-119); x = w * select(w > 0, v, 0)
+    double wsum = 0.0;
+    if constexpr (MODE == 0) {
+        const int myrank = fd->rank[blk];
+        const IT *img = reinterpret_cast<const IT *>(fd->image);
+        for (int idx = t; idx < M * N; idx += NT) {
+            const int i = idx / N, j = idx - i * N;
+            const int y = wr0 + i, x = wc0 + j;
+            const uint8_t s = fd->mask[(size_t)y * A.W + x];
+            const double dec = A.decay[abs(2 * i - (M - 1)) * A.decay_dim + abs(2 * j - (N - 1))];
+            double w;
+            if (s == FSE_LOST) {
+                const int owner = (y / A.B) * A.cols + x / A.B;
+                // R iff the owner block was written by an earlier batch
+                // (snapshot semantics, conceal.py:148-163); BI/BO otherwise
+                w = (owner != blk && fd->rank[owner] < myrank) ? A.delta * dec : 0.0;
+            } else if (s == FSE_RECONSTRUCTED) {
+                w = A.delta * dec;
+            } else {
+                w = dec;
+            }
+            const double v = (double)img[(size_t)y * A.W + x];
+            xs[idx] = w > 0.0 ? (T)(w * v) : (T)0;
+            ws[idx] = (T)w;
+            wsum += w;
+        }
+    } else {
+        const T *val = reinterpret_cast<const T *>(A.values) + (size_t)entry_idx * M * N;
+        const T *wgt = reinterpret_cast<const T *>(A.weights) + (size_t)entry_idx * M * N;
+        for (int idx = t; idx < M * N; idx += NT) {
+            const double w = (double)wgt[idx];
+            const double r0 = w > 0.0 ? (double)val[idx] : 0.0;
+            xs[idx] = (T)(w * r0);
+            ws[idx] = (T)w;
+            wsum += w;
+        }
+    }
+    for (int off = 16; off; off >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, off);
+    if (lane == 0) red[warp] = wsum;
+    __syncthreads();
+    double total = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) total += red[w];
+
+    // ---- DFT pass 1 (columns): Y[k1][n] = sum_m x[m][n] e^{-j 2 pi k1 m / F}, k1 <= F/2
+    for (int o = t; o < R1 * N; o += NT) {
+        const int k1 = o / N, n = o - k1 * N;
+        T xr = 0, xi = 0, wr = 0, wi = 0;
+        int k = 0;
+        for (int m = 0; m < M; ++m) {
+            const T2 tv = tw[k];
+            const T xv = xs[m * N + n], wv = ws[m * N + n];
+            xr = fma(xv, tv.x, xr);
+            xi = fma(-xv, tv.y, xi);
+            wr = fma(wv, tv.x, wr);
+            wi = fma(-wv, tv.y, wi);
+            k = (k + k1) & (F - 1);
+        }
+        Yx[o] = T2{xr, xi};
+        Yw[o] = T2{wr, wi};
+    }
+    __syncthreads();
+
+    // ---- bin ownership: warp w owns row segments w + NW*j: row u0 + RSTEP*j,
+    // columns seg*32 + lane.
+    const int seg = warp % SEG;
+    const int u0 = warp / SEG;
+    const int v = seg * 32 + lane;
+
+    // ---- DFT pass 2 (rows), fused for x and w: g (canonical bins) into
+    // registers, W half-plane rows into ext rows F/2 .. F.
+    T gr[NB], gi[NB];
+    unsigned valid = 0;  // bit j: bin j is a canonical in-range bin
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+        const int u = u0 + RSTEP * j;
+        gr[j] = (T)0;
+        gi[j] = (T)0;
+        if (u < R1) {
+            const T2 *yx = Yx + u * N, *yw = Yw + u * N;
+            T ar = 0, ai = 0, br = 0, bi = 0;
+            int k = 0;
+            for (int n = 0; n < N; ++n) {
+                const T2 tv = tw[k], a = yx[n], b = yw[n];
+                ar = fma(a.x, tv.x, fma(a.y, tv.y, ar));
+                ai = fma(a.y, tv.x, fma(-a.x, tv.y, ai));
+                br = fma(b.x, tv.x, fma(b.y, tv.y, br));
+                bi = fma(b.y, tv.x, fma(-b.x, tv.y, bi));
+                k = (k + v) & (F - 1);
+            }
+            Wext[(u + F / 2) * F + v] = T2{br, bi};
+            const bool canon = !((u == 0 || u == F / 2) && v > F / 2);
+            if (canon) {
+                gr[j] = ar;
+                gi[j] = ai;
+                valid |= 1u << j;
+            }
+        }
+    }
+    __syncthreads();
+    // extension rows: W[-s] = conj W[s] reflected, W[F] = W[0]
+    for (int idx = t; idx < (F / 2) * F; idx += NT) {
+        const int rr = idx / F, c = idx - rr * F;  // ext row rr in [0, F/2): W row rr - F/2
+        const int s = F / 2 - rr;                  // W row -s, s in [1, F/2]
+        const T2 src = Wext[(s + F / 2) * F + ((F - c) & (F - 1))];
+        Wext[rr * F + c] = T2{src.x, -src.y};
+    }
+    for (int idx = t; idx < (F / 2) * F; idx += NT) {
+        const int rr = F + 1 + idx / F, c = idx % F;  // ext row rr in (F, 3F/2]: W row rr - F/2
+        const int s = rr - F / 2;                     // in (F/2, F]
+        T2 val;
+        if (s == F) {
+            val = Wext[(F / 2) * F + c];
+        } else {
+            const T2 src = Wext[(F - s + F / 2) * F + ((F - c) & (F - 1))];
+            val = T2{src.x, -src.y};
+        }
+        Wext[rr * F + c] = val;
+    }
+    __syncthreads();
+
+    // model samples of the block owned by this thread (q = t, t + NT)
+    T mval[2] = {(T)0, (T)0};
+    int mi[2] = {0, 0}, mj[2] = {0, 0};
+    bool mown[2] = {false, false};
+    if constexpr (MODE == 0) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int q = t + k * NT;
+            mown[k] = q < bh * bw;
+            if (mown[k]) {
+                mi[k] = br0 + q / bw;
+                mj[k] = bc0 + q % bw;
+            }
+        }
+    }
+    const T gamma = (T)A.gamma;
+    const T tot = (T)total;
+    const T inv_tot = (T)1 / tot;
+    const int I = A.iterations;
+    int32_t *picks_out = nullptr;
+    T *plog = nullptr;
+    if constexpr (MODE == 0) {
+        if (A.picks) picks_out = A.picks + ((size_t)frame * A.rows * A.cols + blk) * (size_t)I * 2;
+    } else {
+        picks_out = A.picks + (size_t)entry_idx * I * 2;
+        plog = reinterpret_cast<T *>(A.plog) + (size_t)entry_idx * I * 2;
+    }
+
+    // ---- per-thread argmax state over the owned bins
+    // fp32: packed 32-bit keys (energy bits with a 4-bit bin tag, larger =
+    // better, smaller j wins ties), top-2 for the guard.  fp64: exact energy.
+    unsigned k1 = 0, k2 = 0;
+    T best = (T)-1;
+    int bj = -1;
+    auto track = [&](int j, T e) {
+        if constexpr (IS_F32 && GUARD) {
+            const unsigned key = (__float_as_uint((float)e) & ~0x1Fu) | (unsigned)(31 - j);
+            k2 = max(k2, min(k1, key));
+            k1 = max(k1, key);
+        } else {
+            if (e > best) {
+                best = e;
+                bj = j;
+            }
+        }
+    };
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+        if ((valid >> j) & 1u) track(j, gr[j] * gr[j] + gi[j] * gi[j]);
+
+    for (int it = 0; it < I; ++it) {
+        // ---- (1) CTA-wide argmax (+ runner-up for the guard), one barrier
+        FastSlot *sl = slots + (it & 1) * NW;
+        if constexpr (IS_F32 && GUARD) {
+            const unsigned w1 = warp_max_u32(k1);
+            const int wl = __ffs(__ballot_sync(0xffffffffu, k1 == w1)) - 1;
+            const unsigned w2 = warp_max_u32(lane == wl ? k2 : k1);
+            if (lane == wl) {
+                const int jj = 31 - (int)(k1 & 0x1Fu);
+                T pr = (T)0, pi = (T)0;
+#pragma unroll
+                for (int j = 0; j < NB; ++j)
+                    if (j == jj) {
+                        pr = gr[j];
+                        pi = gi[j];
+                    }
+                const unsigned lin = (unsigned)((u0 + RSTEP * jj) * F + v);
+                sl[warp].key = k1 ? (((unsigned long long)(w1 >> 5) << 32) | (0xFFFFFFFFu - lin)) : 0ull;
+                sl[warp].second = w2;
+                sl[warp].pre = (double)pr;
+                sl[warp].pim = (double)pi;
+            }
+        } else {
+            int lin = 0x7FFFFFFF;
+#pragma unroll
+            for (int j = 0; j < NB; ++j)
+                if (j == bj) lin = (u0 + RSTEP * j) * F + v;
+            const unsigned long long key = bj >= 0 ? pack_key(best, lin) : 0ull;
+            const unsigned long long wkey = warp_max_key(key);
+            const int wl = __ffs(__ballot_sync(0xffffffffu, key == wkey)) - 1;
+            if (lane == wl) {
+                T pr = (T)0, pi = (T)0;
+#pragma unroll
+                for (int j = 0; j < NB; ++j)
+                    if (j == bj) {
+                        pr = gr[j];
+                        pi = gi[j];
+                    }
+                sl[warp].key = wkey;
+                sl[warp].pre = (double)pr;
+                sl[warp].pim = (double)pi;
+            }
+        }
+        __syncthreads();
+        const unsigned long long uk = lane < NW ? sl[lane].key : 0ull;
+        const unsigned long long gk = warp_max_key(uk);
+        const int gw = __ffs(__ballot_sync(0xffffffffu, uk == gk)) - 1;
+        int a, b;
+        if constexpr (IS_F32 && GUARD) {
+            const int lin = (int)(0xFFFFFFFFu - (unsigned)(gk & 0xFFFFFFFFull));
+            a = lin / F;
+            b = lin - a * F;
+            // runner-up energy key: best of the other warps, or the winner warp's second
+            const unsigned cand = lane < NW ? (lane == gw ? sl[lane].second : (unsigned)(sl[lane].key >> 32) << 5)
+                                            : 0u;
+            const unsigned g2 = warp_max_u32(cand);
+            const float e1 = __uint_as_float((unsigned)(gk >> 32) << 5);
+            const float e2 = __uint_as_float(g2 & ~0x1Fu);
+            const float tau = A.tau0 + A.tau1 * (float)it;
+            if constexpr (MODE == 0) {
+                if (e1 - e2 <= tau * e1) {
+                    // near tie: hand the window to the fp64 kernel (uniform exit)
+                    if (t == 0) {
+                        const int q = atomicAdd(A.redo_count, 1);
+                        A.redo_list[q] = entry;
+                    }
+                    return;
+                }
+            }
+        } else {
+            const int lin = 0xFFFF - (int)(gk & 0xFFFFull);
+            a = lin / F;
+            b = lin - a * F;
+        }
+        // p = g[a,b] / sum(w) (_kernel.pyx:46-47); fp32 multiplies by 1/sum(w)
+        T pre, pim;
+        if constexpr (IS_F32) {
+            pre = (T)sl[gw].pre * inv_tot;
+            pim = (T)sl[gw].pim * inv_tot;
+        } else {
+            pre = (T)sl[gw].pre / tot;
+            pim = (T)sl[gw].pim / tot;
+        }
+        const bool selfc = ((2 * a) & (F - 1)) == 0 && ((2 * b) & (F - 1)) == 0;
+        if (t == 0 && picks_out) {
+            picks_out[2 * it] = a;
+            picks_out[2 * it + 1] = b;
+            if constexpr (MODE == 1) {
+                plog[2 * it] = pre;
+                plog[2 * it + 1] = pim;
+            }
+        }
+        // self-conjugate: gamma * Re(p) * W[k - j] == (gamma Re(p) / 2) (W[k-j] + W[k+j])
+        T gpr = gamma * pre, gpi = gamma * pim;
+        if (selfc) {
+            gpr = gpr * (T)0.5;
+            gpi = (T)0;
+        }
+
+        // ---- (2) model over the block: 2 Re(gp e^{+j 2 pi (a i + b j)/F}) (fse.py:159)
+        if constexpr (MODE == 0) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+                if (mown[k]) {
+                    const T2 ph = tw[(a * mi[k] + b * mj[k]) & (F - 1)];
+                    mval[k] += (T)2 * (gpr * ph.x - gpi * ph.y);
+                }
+        }
+        if (it + 1 == I) break;  // the last spectrum update is never observed
+
+        // ---- (3) spectrum update by the shifted weight spectrum + next argmax
+        const int cm = (v - b) & (F - 1), cp = (v + b) & (F - 1);
+        const T2 *lo = Wext + (u0 - a + F / 2) * F + cm;
+        const T2 *hi = Wext + (u0 + a + F / 2) * F + cp;
+        k1 = 0;
+        k2 = 0;
+        best = (T)-1;
+        bj = -1;
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+            const bool inr = (j < NB - 1) || (C::NSEGS % NW == 0) || (u0 + RSTEP * j < R1);
+            if (inr) {
+                const T2 l = lo[j * RSTEP * F], h = hi[j * RSTEP * F];
+                const T sA = l.x + h.x, sB = l.y - h.y, sC = l.y + h.y, sD = l.x - h.x;
+                gr[j] = fma(gpi, sB, fma(-gpr, sA, gr[j]));
+                gi[j] = fma(-gpi, sD, fma(-gpr, sC, gi[j]));
+                const T e = gr[j] * gr[j] + gi[j] * gi[j];
+                if (j == 0 || j == NB - 1) {
+                    if ((valid >> j) & 1u) track(j, e);
+                } else {
+                    track(j, e);
+                }
+            }
+        }
+    }
+
+    // ---- write-back of the block's LOST samples (conceal.py:61-66)
+    if constexpr (MODE == 0) {
+        IT *img = reinterpret_cast<IT *>(fd->image);
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+            if (mown[k]) {
+                const size_t off = (size_t)(wr0 + mi[k]) * A.W + (wc0 + mj[k]);
+                if (fd->mask[off] == FSE_LOST) img[off] = (IT)mval[k];
+            }
+    }
+}
+
+template <class C, int MODE, bool GUARD>
+__global__ void __launch_bounds__(C::NT) fse_fast_kernel(const FastArgs A, const FastLayout L) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    fast_window<C, MODE, GUARD, typename C::T>(A, L, blockIdx.x, sm);
+}
+
+// Persistent variant over a device-side list (the fp64 redo of guarded windows
+// of an fp32 image: IT = float, compute type C::T = double).
+template <class C, typename IT>
+__global__ void __launch_bounds__(C::NT) fse_fast_redo_kernel(const FastArgs A, const FastLayout L) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    const int n = *A.count;
+    for (int e = blockIdx.x; e < n; e += gridDim.x) {
+        fast_window<C, 0, false, IT>(A, L, e, sm);
+        __syncthreads();
+    }
+}
+
+// Host launchers (fse_inst_fast.cu).  dtype FSE_F32/FSE_F64, F = 32/64.
+int fast_supported(int F, int Mmax, int Nmax, int model_n);
+int fast_level(int dtype, int F, bool guard, const FastArgs &a, int grid, int Mmax, int Nmax,
+               int model_n, cudaStream_t s);
+int fast_redo(int F, const FastArgs &a, int max_entries, int Mmax, int Nmax, int model_n,
+              cudaStream_t s);
+int fast_windows(int dtype, int F, const FastArgs &a, int grid, cudaStream_t s);
+
+}  // namespace fse
