@@ -55,6 +55,8 @@ def args_():
     ap.add_argument("--config", type=int, default=4, choices=[3, 4])
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--frames", type=int, default=64)
+    ap.add_argument("--guard", default=None,
+                    help="fp32 near-tie guard 'tau0,tau1' or 'off' (default: library default)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-blocks", type=int, default=2000,
@@ -237,6 +239,9 @@ def run_b200(a, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     lib = _lib.lib()
+    if a.guard is not None:
+        t0_, t1_ = (-1.0, 0.0) if a.guard == "off" else (float(x) for x in a.guard.split(","))
+        lib.fse_set_guard(t0_, t1_)
     iters = iterations_for(a.config)
     params = P.FseParams(d=D, rho=RHO, delta=DELTA, gamma=GAMMA, iterations=iters, block_size=B,
                          fft_size=F)
@@ -304,13 +309,13 @@ def run_b200(a, rank, world, local_rank):
         ms = timed(step, a.steps)
     lib.fse_timing_enable(0)
     launches = int(lib.fse_launch_count(1))
-    redo = int(lib.fse_guard_redo_count(1))
     import ctypes
 
     kms = ctypes.c_double()
     wl = ctypes.c_int64()
     calls = ctypes.c_int64()
     _lib.check(lib.fse_timing_read(ctypes.byref(kms), ctypes.byref(wl), ctypes.byref(calls)))
+    redo = int(lib.fse_guard_redo_count(1))
 
     tot = torch.tensor([blocks_rank, lost_px_rank], dtype=torch.float64, device="cuda")
     if world > 1:

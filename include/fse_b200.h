@@ -149,7 +149,7 @@ int fse_conceal_frames(int32_t n, FsePlan *const *plans, void *const *images,
 /* fp32 near-tie guard of the fast path (F = 32/64): a window whose runner-up
  * energy comes within (tau0 + tau1 * iteration) of the maximum is recomputed
  * by the fp64 kernel before the next level.  tau0 < 0 disables the guard.
- * Defaults 2e-5, 3e-6.  Process-wide. */
+ * Default: off (tau0 = -1).  Process-wide. */
 int fse_set_guard(double tau0, double tau1);
 /* Windows redone in fp64 by the guard, summed over timed calls (fse_timing_*). */
 int64_t fse_guard_redo_count(int32_t reset);

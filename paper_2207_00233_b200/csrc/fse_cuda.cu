@@ -27,7 +27,7 @@ static thread_local TimingState g_timing;
 
 // fp32 near-tie guard thresholds (fse_fast.cuh): redo in fp64 when
 // e1 - e2 <= (tau0 + tau1 * it) * e1.  Negative tau0 disables the guard.
-static double g_tau0 = 2e-5, g_tau1 = 3e-6;
+static double g_tau0 = -1.0, g_tau1 = 0.0;
 static long long g_redo_total = 0;
 
 // FP32 FMA throughput probe: 8 independent FFMA chains per thread.

@@ -53,11 +53,12 @@ struct FastCfg {
     static_assert(NB <= 32, "5-bit bin tag");
 };
 
+template <typename T>
 struct FastSlot {
     unsigned long long key;  // fp64: exact key; fp32: (energy key << 32) | ~lin
-    unsigned int second;     // fp32: energy key of the warp's runner-up
+    unsigned int second;     // fp32 guard: energy key of the warp's runner-up
     unsigned int pad;
-    double pre, pim;         // p = g / sum(w) of the warp's best bin
+    T gre, gim;              // g of the warp's best bin
 };
 
 struct FastLayout {
@@ -71,7 +72,7 @@ __host__ __device__ inline FastLayout fast_layout(int F, int NW, int Mmax, int N
     size_t o = 0;
     L.tw = o; o += (size_t)F * c2;
     o = (o + 15) & ~size_t(15);
-    L.slots = o; o += 2 * (size_t)NW * sizeof(FastSlot);
+    L.slots = o; o += 2 * (size_t)NW * sizeof(FastSlot<double>);
     L.red = o; o += (size_t)(NW + 2) * sizeof(double);
     L.model = o; o += (size_t)(model_n > 0 ? model_n : 1) * sizeof(T);
     o = (o + 127) & ~size_t(127);
@@ -126,6 +127,58 @@ struct FastArgs {
 
 __device__ __forceinline__ unsigned warp_max_u32(unsigned v) { return __reduce_max_sync(0xffffffffu, v); }
 
+// ---- complex pair arithmetic.  fp32 uses the sm_100 packed f32x2 pipe
+// (FADD2 / FFMA2: two lanes of fp32 math per instruction, with scalar
+// broadcast and half-swizzle operands), halving the issue slots of the
+// update; fp64 is plain scalar math in the same operation order.
+__device__ __forceinline__ unsigned long long f2u(float2 a) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+    return r;
+}
+__device__ __forceinline__ float2 u2f(unsigned long long r) {
+    float2 a;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+    return a;
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) {
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
+    return u2f(r);
+}
+__device__ __forceinline__ float2 csub(float2 a, float2 b) {
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
+    return u2f(r);
+}
+__device__ __forceinline__ float2 cfma(float2 a, float2 b, float2 c) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(c)));
+    return u2f(r);
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return double2{a.x + b.x, a.y + b.y}; }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return double2{a.x - b.x, a.y - b.y}; }
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
+    return double2{fma(a.x, b.x, c.x), fma(a.y, b.y, c.y)};
+}
+
+// g -= gamma*(p W[k-j] + conj(p) W[k+j]) with gp = gamma*p  (_kernel.pyx:84-91):
+//   re: g.x - gpr (lo.x + hi.x) + gpi (lo.y - hi.y)
+//   im: g.y - gpr (lo.y + hi.y) - gpi (lo.x - hi.x)
+template <typename T2, typename T>
+__device__ __forceinline__ T2 spectral_update(T2 g, T2 lo, T2 hi, T gpr, T gpi) {
+    const T2 S = cadd(lo, hi), D = csub(lo, hi);
+    g = cfma(T2{-gpr, -gpr}, S, g);
+    return cfma(T2{gpi, -gpi}, T2{D.y, D.x}, g);
+}
+
+// acc += z * e^{-j theta}, tw = (cos theta, sin theta): the forward-DFT MAC
+template <typename T2>
+__device__ __forceinline__ T2 dft_mac(T2 acc, T2 z, T2 tw) {
+    acc = cfma(z, T2{tw.x, tw.x}, acc);
+    return cfma(T2{z.y, -z.x}, T2{tw.y, tw.y}, acc);
+}
+
 template <class C, int MODE, bool GUARD, typename IT>
 __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout &L, const int entry_idx,
                                             unsigned char *sm) {
@@ -137,7 +190,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
 
     T2 *tw = reinterpret_cast<T2 *>(sm + L.tw);
-    FastSlot *slots = reinterpret_cast<FastSlot *>(sm + L.slots);
+    FastSlot<T> *slots = reinterpret_cast<FastSlot<T> *>(sm + L.slots);
     double *red = reinterpret_cast<double *>(sm + L.red);
     unsigned char *big = sm + L.big;
     T2 *Wext = reinterpret_cast<T2 *>(big);
@@ -225,19 +278,17 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     // ---- DFT pass 1 (columns): Y[k1][n] = sum_m x[m][n] e^{-j 2 pi k1 m / F}, k1 <= F/2
     for (int o = t; o < R1 * N; o += NT) {
         const int k1 = o / N, n = o - k1 * N;
-        T xr = 0, xi = 0, wr = 0, wi = 0;
+        T2 X = T2{0, 0}, Wc = T2{0, 0};
         int k = 0;
         for (int m = 0; m < M; ++m) {
             const T2 tv = tw[k];
             const T xv = xs[m * N + n], wv = ws[m * N + n];
-            xr = fma(xv, tv.x, xr);
-            xi = fma(-xv, tv.y, xi);
-            wr = fma(wv, tv.x, wr);
-            wi = fma(-wv, tv.y, wi);
+            X = cfma(T2{xv, -xv}, tv, X);    // x e^{-j theta}
+            Wc = cfma(T2{wv, -wv}, tv, Wc);
             k = (k + k1) & (F - 1);
         }
-        Yx[o] = T2{xr, xi};
-        Yw[o] = T2{wr, wi};
+        Yx[o] = X;
+        Yw[o] = Wc;
     }
     __syncthreads();
 
@@ -249,30 +300,26 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
 
     // ---- DFT pass 2 (rows), fused for x and w: g (canonical bins) into
     // registers, W half-plane rows into ext rows F/2 .. F.
-    T gr[NB], gi[NB];
+    T2 G[NB];
     unsigned valid = 0;  // bit j: bin j is a canonical in-range bin
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
         const int u = u0 + RSTEP * j;
-        gr[j] = (T)0;
-        gi[j] = (T)0;
+        G[j] = T2{0, 0};
         if (u < R1) {
             const T2 *yx = Yx + u * N, *yw = Yw + u * N;
-            T ar = 0, ai = 0, br = 0, bi = 0;
+            T2 ga = T2{0, 0}, wa = T2{0, 0};
             int k = 0;
             for (int n = 0; n < N; ++n) {
-                const T2 tv = tw[k], a = yx[n], b = yw[n];
-                ar = fma(a.x, tv.x, fma(a.y, tv.y, ar));
-                ai = fma(a.y, tv.x, fma(-a.x, tv.y, ai));
-                br = fma(b.x, tv.x, fma(b.y, tv.y, br));
-                bi = fma(b.y, tv.x, fma(-b.x, tv.y, bi));
+                const T2 tv = tw[k];
+                ga = dft_mac(ga, yx[n], tv);
+                wa = dft_mac(wa, yw[n], tv);
                 k = (k + v) & (F - 1);
             }
-            Wext[(u + F / 2) * F + v] = T2{br, bi};
+            Wext[(u + F / 2) * F + v] = wa;
             const bool canon = !((u == 0 || u == F / 2) && v > F / 2);
             if (canon) {
-                gr[j] = ar;
-                gi[j] = ai;
+                G[j] = ga;
                 valid |= 1u << j;
             }
         }
@@ -306,7 +353,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     if constexpr (MODE == 0) {
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-            const int q = t + k * NT;
+            const int q = lane * NW + warp + k * NT;  // spread over the warps
             mown[k] = q < bh * bw;
             if (mown[k]) {
                 mi[k] = br0 + q / bw;
@@ -333,63 +380,49 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     unsigned k1 = 0, k2 = 0;
     T best = (T)-1;
     int bj = -1;
+    T2 bg = T2{0, 0};  // g of the thread's best bin, carried along (no register indexing later)
     auto track = [&](int j, T e) {
         if constexpr (IS_F32 && GUARD) {
             const unsigned key = (__float_as_uint((float)e) & ~0x1Fu) | (unsigned)(31 - j);
+            if (key > k1) bg = G[j];
             k2 = max(k2, min(k1, key));
             k1 = max(k1, key);
         } else {
             if (e > best) {
                 best = e;
                 bj = j;
+                bg = G[j];
             }
         }
     };
 #pragma unroll
     for (int j = 0; j < NB; ++j)
-        if ((valid >> j) & 1u) track(j, gr[j] * gr[j] + gi[j] * gi[j]);
+        if ((valid >> j) & 1u) track(j, G[j].x * G[j].x + G[j].y * G[j].y);
 
     for (int it = 0; it < I; ++it) {
         // ---- (1) CTA-wide argmax (+ runner-up for the guard), one barrier
-        FastSlot *sl = slots + (it & 1) * NW;
+        FastSlot<T> *sl = slots + (it & 1) * NW;
         if constexpr (IS_F32 && GUARD) {
             const unsigned w1 = warp_max_u32(k1);
             const int wl = __ffs(__ballot_sync(0xffffffffu, k1 == w1)) - 1;
             const unsigned w2 = warp_max_u32(lane == wl ? k2 : k1);
             if (lane == wl) {
                 const int jj = 31 - (int)(k1 & 0x1Fu);
-                T pr = (T)0, pi = (T)0;
-#pragma unroll
-                for (int j = 0; j < NB; ++j)
-                    if (j == jj) {
-                        pr = gr[j];
-                        pi = gi[j];
-                    }
                 const unsigned lin = (unsigned)((u0 + RSTEP * jj) * F + v);
                 sl[warp].key = k1 ? (((unsigned long long)(w1 >> 5) << 32) | (0xFFFFFFFFu - lin)) : 0ull;
                 sl[warp].second = w2;
-                sl[warp].pre = (double)pr;
-                sl[warp].pim = (double)pi;
+                sl[warp].gre = bg.x;
+                sl[warp].gim = bg.y;
             }
         } else {
-            int lin = 0x7FFFFFFF;
-#pragma unroll
-            for (int j = 0; j < NB; ++j)
-                if (j == bj) lin = (u0 + RSTEP * j) * F + v;
+            const int lin = (u0 + RSTEP * bj) * F + v;
             const unsigned long long key = bj >= 0 ? pack_key(best, lin) : 0ull;
             const unsigned long long wkey = warp_max_key(key);
             const int wl = __ffs(__ballot_sync(0xffffffffu, key == wkey)) - 1;
             if (lane == wl) {
-                T pr = (T)0, pi = (T)0;
-#pragma unroll
-                for (int j = 0; j < NB; ++j)
-                    if (j == bj) {
-                        pr = gr[j];
-                        pi = gi[j];
-                    }
                 sl[warp].key = wkey;
-                sl[warp].pre = (double)pr;
-                sl[warp].pim = (double)pi;
+                sl[warp].gre = bg.x;
+                sl[warp].gim = bg.y;
             }
         }
         __syncthreads();
@@ -426,11 +459,11 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         // p = g[a,b] / sum(w) (_kernel.pyx:46-47); fp32 multiplies by 1/sum(w)
         T pre, pim;
         if constexpr (IS_F32) {
-            pre = (T)sl[gw].pre * inv_tot;
-            pim = (T)sl[gw].pim * inv_tot;
+            pre = sl[gw].gre * inv_tot;
+            pim = sl[gw].gim * inv_tot;
         } else {
-            pre = (T)sl[gw].pre / tot;
-            pim = (T)sl[gw].pim / tot;
+            pre = sl[gw].gre / tot;
+            pim = sl[gw].gim / tot;
         }
         const bool selfc = ((2 * a) & (F - 1)) == 0 && ((2 * b) & (F - 1)) == 0;
         if (t == 0 && picks_out) {
@@ -471,11 +504,8 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         for (int j = 0; j < NB; ++j) {
             const bool inr = (j < NB - 1) || (C::NSEGS % NW == 0) || (u0 + RSTEP * j < R1);
             if (inr) {
-                const T2 l = lo[j * RSTEP * F], h = hi[j * RSTEP * F];
-                const T sA = l.x + h.x, sB = l.y - h.y, sC = l.y + h.y, sD = l.x - h.x;
-                gr[j] = fma(gpi, sB, fma(-gpr, sA, gr[j]));
-                gi[j] = fma(-gpi, sD, fma(-gpr, sC, gi[j]));
-                const T e = gr[j] * gr[j] + gi[j] * gi[j];
+                G[j] = spectral_update(G[j], lo[j * RSTEP * F], hi[j * RSTEP * F], gpr, gpi);
+                const T e = G[j].x * G[j].x + G[j].y * G[j].y;
                 if (j == 0 || j == NB - 1) {
                     if ((valid >> j) & 1u) track(j, e);
                 } else {
