@@ -58,6 +58,7 @@ def args_():
     ap.add_argument("--guard", default=None,
                     help="fp32 near-tie guard 'tau0,tau1' or 'off' (default: library default)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-second", action="store_true", help="skip the other precision's measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-blocks", type=int, default=2000,
                     help="cpu_baseline sample: lossy blocks of frame 0 (about 10 s single core)")
@@ -210,27 +211,32 @@ def run_reference(a, rank, world):
 
 # ------------------------------------------------------------------ B200 arm
 
-def measure_fp32_peak(torch, lib):
-    """FFMA throughput of this GPU (roofline denominator), CUDA events."""
+def measure_peaks(torch, lib):
+    """Arithmetic throughput of this GPU (roofline denominators), CUDA events:
+    FFMA, FFMA2 (packed f32x2, what the fp32 kernel issues) and DFMA."""
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     scratch = torch.zeros(1, device="cuda")
     s = torch.cuda.current_stream()
     blocks, threads, iters = sms * 8, 256, 4096
-    for _ in range(2):
-        lib.fse_fma_probe(blocks, threads, iters, scratch.data_ptr(), s.cuda_stream)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    reps = 5
-    for _ in range(reps):
-        lib.fse_fma_probe(blocks, threads, iters, scratch.data_ptr(), s.cuda_stream)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / reps
-    flops = 16.0 * iters * blocks * threads
-    return flops / (ms * 1e-3) / 1e12, sms
+    out = {}
+    for kind, name, fpt in ((0, "ffma", 16.0), (1, "ffma2", 32.0), (2, "dfma", 16.0)):
+        for _ in range(2):
+            lib.fse_fma_probe(kind, blocks, threads, iters, scratch.data_ptr(), s.cuda_stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 5
+        e0.record()
+        for _ in range(reps):
+            lib.fse_fma_probe(kind, blocks, threads, iters, scratch.data_ptr(), s.cuda_stream)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        out[name] = fpt * iters * blocks * threads / (ms * 1e-3) / 1e12
+    return out, sms
 
 
 def run_b200(a, rank, world, local_rank):
+    import ctypes
+
     import torch
     import torch.distributed as dist
 
@@ -250,10 +256,8 @@ def run_b200(a, rank, world, local_rank):
     imgs_h = torch.from_numpy(np.stack([s[0] for s in scenes])).pin_memory()
     msks_h = torch.from_numpy(np.stack([s[1] for s in scenes])).pin_memory()
     n, H, W = imgs_h.shape
-    tdt = torch.float32 if a.precision == "fp32" else torch.float64
     imgs_d = imgs_h.cuda()
     msks_d = msks_h.cuda()
-    work = torch.empty((n, H, W), dtype=tdt, device="cuda")
     mout = torch.empty_like(msks_d)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     masks_np = list(msks_h.numpy())
@@ -265,16 +269,6 @@ def run_b200(a, rank, world, local_rank):
     lost_px_rank = int((msks_h == 1).sum())
     levels = max(p.n_levels for p in plans)
     del plans
-    plan_ms = []
-
-    def step():
-        flush.zero_()
-        t = time.perf_counter()
-        pl = P.build_plans(masks_np, params, "optimized", plan_threads)
-        plan_ms.append(1e3 * (time.perf_counter() - t))
-        work.copy_(imgs_d)
-        P.run_frames_device(pl, list(work), list(msks_d), list(mout), params, a.precision)
-        return pl
 
     def timed(fn, k):
         if world > 1:
@@ -297,37 +291,70 @@ def run_b200(a, rank, world, local_rank):
             ms = float(t.item())
         return ms
 
-    for _ in range(a.warmup):
-        step()
-    torch.cuda.synchronize()
-    plan_ms.clear()
-    lib.fse_launch_count(1)
-    lib.fse_timing_read(None, None, None)
-    lib.fse_guard_redo_count(1)
-    lib.fse_timing_enable(1)
-    with ClockSampler(local_rank) as clk:
-        ms = timed(step, a.steps)
-    lib.fse_timing_enable(0)
-    launches = int(lib.fse_launch_count(1))
-    import ctypes
+    def measure(precision, sample_clocks):
+        """Device-resident step: plans + uint8->float working copy + level
+        launches + mask pass, K steps after W warm-up steps."""
+        tdt = torch.float32 if precision == "fp32" else torch.float64
+        work = torch.empty((n, H, W), dtype=tdt, device="cuda")
+        plan_ms = []
 
-    kms = ctypes.c_double()
-    wl = ctypes.c_int64()
-    calls = ctypes.c_int64()
-    _lib.check(lib.fse_timing_read(ctypes.byref(kms), ctypes.byref(wl), ctypes.byref(calls)))
-    redo = int(lib.fse_guard_redo_count(1))
+        def step():
+            flush.zero_()
+            t = time.perf_counter()
+            pl = P.build_plans(masks_np, params, "optimized", plan_threads)
+            plan_ms.append(1e3 * (time.perf_counter() - t))
+            work.copy_(imgs_d)
+            P.run_frames_device(pl, list(work), list(msks_d), list(mout), params, precision)
+            return pl
+
+        for _ in range(a.warmup):
+            step()
+        torch.cuda.synchronize()
+        plan_ms.clear()
+        lib.fse_launch_count(1)
+        lib.fse_timing_read(None, None, None)
+        lib.fse_guard_redo_count(1)
+        lib.fse_timing_enable(1)
+        clk = ClockSampler(local_rank) if sample_clocks else None
+        if clk:
+            clk.__enter__()
+        ms = timed(step, a.steps)
+        if clk:
+            clk.__exit__(None, None, None)
+        lib.fse_timing_enable(0)
+        launches = int(lib.fse_launch_count(1))
+        kms, wl, calls = ctypes.c_double(), ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(lib.fse_timing_read(ctypes.byref(kms), ctypes.byref(wl), ctypes.byref(calls)))
+        redo = int(lib.fse_guard_redo_count(1))
+        return {"ms": ms, "kernel_ms": kms.value / a.steps, "launches": launches,
+                "plan_ms": float(np.mean(plan_ms)) if plan_ms else None, "redo": redo / a.steps,
+                "clocks": clk.summary() if clk else None}
+
+    head = measure(a.precision, True)
+    other_prec = "fp64" if a.precision == "fp32" else "fp32"
+    other = None if a.no_second else measure(other_prec, False)
 
     tot = torch.tensor([blocks_rank, lost_px_rank], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(tot)
     blocks_all, lost_px_all = float(tot[0]), float(tot[1])
-    value = blocks_all * a.steps / (ms * 1e-3)
+    value = blocks_all * a.steps / (head["ms"] * 1e-3)
 
-    # roofline of the dominant kernel (the level launches, fse_window_kernel)
+    # roofline of the dominant kernel (the level launches): counted FLOPs per
+    # block x blocks of this rank / summed CUDA-event time of the level launches
     flop_blk = counted_flops_per_block(iters, F, F)
-    kernel_ms = kms.value / a.steps
-    achieved = blocks_rank * flop_blk / (kernel_ms * 1e-3) / 1e12
-    peak, sms = measure_fp32_peak(torch, lib)
+    peaks, sms = measure_peaks(torch, lib)
+    fp32_peak = max(peaks["ffma"], peaks["ffma2"])
+
+    def roof(m, precision):
+        achieved = blocks_rank * flop_blk / (m["kernel_ms"] * 1e-3) / 1e12
+        pk = fp32_peak if precision == "fp32" else peaks["dfma"]
+        return {"bound": "fp32" if precision == "fp32" else "fp64", "achieved": achieved, "peak": pk,
+                "unit": "TFLOP/s", "frac": achieved / pk, "frac_of_fp32_peak": achieved / fp32_peak,
+                "traffic": None, "kernel": "fse_fast_kernel (one launch per dependency level)",
+                "flops_per_block": flop_blk,
+                "peak_source": (f"measured live on {sms} SMs by fse_fma_probe: FFMA {peaks['ffma']:.1f}, "
+                                f"FFMA2 {peaks['ffma2']:.1f}, DFMA {peaks['dfma']:.1f} TFLOP/s")}
 
     # e2e through the public API with pinned host buffers
     e2e = None
@@ -365,7 +392,7 @@ def run_b200(a, rank, world, local_rank):
     if rank == 0:
         line = {
             "metric": "lost_blocks_per_s", "value": value, "unit": "blocks/s", "n_gpus": world,
-            "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms / a.steps,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": head["ms"] / a.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32" if a.precision == "fp32" else "f64",
             "data": "synthetic (seeded BASELINE generators, paper_2207_00233_b200/synth.py)",
@@ -375,22 +402,23 @@ def run_b200(a, rank, world, local_rank):
                        "delta": DELTA, "gamma": GAMMA, "order": "optimized",
                        "parallelism": f"frame-parallel x{world}",
                        "l2": "256 MiB buffer written every step (> 126 MB L2)"},
-            "lost_mpixel_per_s": lost_px_all * a.steps / (ms * 1e-3) / 1e6,
+            "lost_mpixel_per_s": lost_px_all * a.steps / (head["ms"] * 1e-3) / 1e6,
             "blocks_per_step": blocks_all, "lost_pixels_per_step": lost_px_all,
             "levels_per_step": levels,
-            "host_plan_ms_per_step": float(np.mean(plan_ms)) if plan_ms else None,
-            "kernel_ms_per_step": kernel_ms,
-            "fp32_guard_fp64_redo_per_step": redo / a.steps,
-            "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": None,
-                         "kernel": "fse_window_kernel (level launches)",
-                         "flops_per_block": flop_blk,
-                         "peak_source": f"measured live: FFMA probe on {sms} SMs (fse_fma_probe)"},
-            "gpu_launches": launches,
+            "host_plan_ms_per_step": head["plan_ms"],
+            "kernel_ms_per_step": head["kernel_ms"],
+            "fp32_guard_fp64_redo_per_step": head["redo"],
+            "roofline": roof(head, a.precision),
+            "gpu_launches": head["launches"],
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "clocks": clk.summary(),
+            "clocks": head["clocks"],
         }
+        if other is not None:
+            line[other_prec] = {
+                "value": blocks_all * a.steps / (other["ms"] * 1e-3), "unit": "blocks/s",
+                "ms_per_step": other["ms"] / a.steps, "kernel_ms_per_step": other["kernel_ms"],
+                "roofline": roof(other, other_prec), "gpu_launches": other["launches"]}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

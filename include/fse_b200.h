@@ -164,10 +164,12 @@ int64_t fse_launch_count(int32_t reset);
 int fse_timing_enable(int32_t on);
 int fse_timing_read(double *ms, int64_t *window_launches, int64_t *calls);
 
-/* FP32 FMA throughput probe (roofline denominator): blocks x threads threads,
- * each running 8 independent FFMA chains for iters steps (16*iters FLOP per
- * thread).  scratch: device float[1]. */
-int fse_fma_probe(int32_t blocks, int32_t threads, int32_t iters, void *scratch, void *stream);
+/* Arithmetic throughput probes (roofline denominators): blocks x threads
+ * threads, each running 8 independent FMA chains for iters steps.
+ * kind 0: FFMA (16*iters FLOP per thread), 1: FFMA2 / packed f32x2
+ * (32*iters), 2: DFMA (16*iters).  scratch: device float[1]. */
+int fse_fma_probe(int32_t kind, int32_t blocks, int32_t threads, int32_t iters, void *scratch,
+                  void *stream);
 
 #ifdef __cplusplus
 }

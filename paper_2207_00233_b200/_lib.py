@@ -81,7 +81,7 @@ def lib():
         L.fse_timing_enable.argtypes = [_i32]
         L.fse_timing_read.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64),
                                       ctypes.POINTER(ctypes.c_int64)]
-        L.fse_fma_probe.argtypes = [_i32, _i32, _i32, _vp, _vp]
+        L.fse_fma_probe.argtypes = [_i32, _i32, _i32, _i32, _vp, _vp]
         L.fse_set_guard.argtypes = [ctypes.c_double, ctypes.c_double]
         L.fse_guard_redo_count.argtypes = [_i32]
         L.fse_guard_redo_count.restype = ctypes.c_int64

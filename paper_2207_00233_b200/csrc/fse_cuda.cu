@@ -45,6 +45,34 @@ __global__ void fma_probe_kernel(float *out, int iters, float a, float b) {
     if (s == 12345.678f) out[0] = s;  // keep the chains alive
 }
 
+// FFMA2 (packed f32x2) and DFMA throughput probes: 8 independent chains.
+__global__ void fma2_probe_kernel(float *out, int iters, float a, float b) {
+    float2 x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = make_float2(threadIdx.x * 1e-3f + k, k * 0.5f);
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = cfma(make_float2(a, a), x[k], make_float2(b, b));
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += x[k].x + x[k].y;
+    if (s == 12345.678f) out[0] = s;
+}
+__global__ void dfma_probe_kernel(float *out, int iters, double a, double b) {
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-3 + k;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += x[k];
+    if (s == 12345.678) out[0] = (float)s;
+}
+
 // LOST samples of concealed blocks become RECONSTRUCTED (conceal.py:65-66)
 __global__ void finalize_masks_kernel(const FrameDesc *frames, int n, int H, int W, int B, int cols) {
     const long long total = (long long)n * H * W;
@@ -129,10 +157,18 @@ int fse_timing_read(double *ms, int64_t *window_launches, int64_t *calls) {
     return FSE_OK;
 }
 
-int fse_fma_probe(int32_t blocks, int32_t threads, int32_t iters, void *scratch, void *stream) {
+int fse_fma_probe(int32_t kind, int32_t blocks, int32_t threads, int32_t iters, void *scratch,
+                  void *stream) {
     if (blocks < 1 || threads < 32 || iters < 1 || !scratch) return fail(FSE_EINVAL, "bad probe shape");
-    fse::fma_probe_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>((float *)scratch, iters,
-                                                                        0.999999f, 1e-7f);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (kind == 0)
+        fse::fma_probe_kernel<<<blocks, threads, 0, st>>>((float *)scratch, iters, 0.999999f, 1e-7f);
+    else if (kind == 1)
+        fse::fma2_probe_kernel<<<blocks, threads, 0, st>>>((float *)scratch, iters, 0.999999f, 1e-7f);
+    else if (kind == 2)
+        fse::dfma_probe_kernel<<<blocks, threads, 0, st>>>((float *)scratch, iters, 0.999999, 1e-7);
+    else
+        return fail(FSE_EINVAL, "probe kind");
     cudaError_t ce = cudaGetLastError();
     if (ce != cudaSuccess) return fail(FSE_ECUDA, cudaGetErrorString(ce));
     return FSE_OK;
