@@ -346,12 +346,24 @@ def run_b200(a, rank, world, local_rank):
     peaks, sms = measure_peaks(torch, lib)
     fp32_peak = max(peaks["ffma"], peaks["ffma2"])
 
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "traffic_r1.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath))
+
     def roof(m, precision):
         achieved = blocks_rank * flop_blk / (m["kernel_ms"] * 1e-3) / 1e12
         pk = fp32_peak if precision == "fp32" else peaks["dfma"]
+        tr = None
+        if traffic and precision == "fp32":
+            tr = {"dram_bytes_per_launch": traffic["dram_bytes_per_launch"],
+                  "launch_blocks": traffic["launch_blocks"],
+                  "dram_bytes_per_block": traffic["dram_bytes_per_block"],
+                  "algorithmic_bytes_per_block": traffic["algorithmic_bytes_per_block"],
+                  "source": traffic["source"]}
         return {"bound": "fp32" if precision == "fp32" else "fp64", "achieved": achieved, "peak": pk,
                 "unit": "TFLOP/s", "frac": achieved / pk, "frac_of_fp32_peak": achieved / fp32_peak,
-                "traffic": None, "kernel": "fse_fast_kernel (one launch per dependency level)",
+                "traffic": tr, "kernel": "fse_fast_kernel (one launch per dependency level)",
                 "flops_per_block": flop_blk,
                 "peak_source": (f"measured live on {sms} SMs by fse_fma_probe: FFMA {peaks['ffma']:.1f}, "
                                 f"FFMA2 {peaks['ffma2']:.1f}, DFMA {peaks['dfma']:.1f} TFLOP/s")}
