@@ -57,7 +57,7 @@ template <typename T>
 struct FastSlot {
     unsigned long long key;  // fp64: exact key; fp32: (energy key << 32) | ~lin
     unsigned int second;     // fp32 guard: energy key of the warp's runner-up
-    unsigned int pad;
+    unsigned int lin;        // row-major index of the warp's best bin
     T gre, gim;              // g of the warp's best bin
 };
 
@@ -126,6 +126,39 @@ struct FastArgs {
 };
 
 __device__ __forceinline__ unsigned warp_max_u32(unsigned v) { return __reduce_max_sync(0xffffffffu, v); }
+__device__ __forceinline__ unsigned warp_min_u32(unsigned v) { return __reduce_min_sync(0xffffffffu, v); }
+
+// Order-preserving unsigned images of IEEE values (for integer REDUX).
+__device__ __forceinline__ unsigned long long ord_key(float e) {
+    const unsigned b = __float_as_uint(e);
+    return (int)b >= 0 ? (b | 0x80000000u) : ~b;
+}
+__device__ __forceinline__ unsigned long long ord_key(double e) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(e);
+    return (long long)b >= 0 ? (b | 0x8000000000000000ull) : ~b;
+}
+
+// Warp argmax of (key, lin): largest key, ties to the smallest lin (the
+// reference's first maximum in row-major order, _kernel.pyx:32-44).  Returns
+// the winning key and lin, uniform across the warp.
+template <typename T>
+__device__ __forceinline__ void warp_argmax(unsigned long long key, unsigned lin, unsigned long long &wkey,
+                                            unsigned &wlin) {
+    bool match;
+    if constexpr (sizeof(T) == 4) {
+        const unsigned k = (unsigned)key;
+        const unsigned m = warp_max_u32(k);
+        match = k == m;
+        wkey = m;
+    } else {
+        const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+        const unsigned mh = warp_max_u32(hi);
+        const unsigned ml = warp_max_u32(hi == mh ? lo : 0u);
+        match = hi == mh && lo == ml;
+        wkey = ((unsigned long long)mh << 32) | ml;
+    }
+    wlin = warp_min_u32(match ? lin : 0xFFFFFFFFu);
+}
 
 // ---- complex pair arithmetic.  fp32 uses the sm_100 packed f32x2 pipe
 // (FADD2 / FFMA2: two lanes of fp32 math per instruction, with scalar
@@ -415,22 +448,24 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
                 sl[warp].gim = bg.y;
             }
         } else {
-            const int lin = (u0 + RSTEP * bj) * F + v;
-            const unsigned long long key = bj >= 0 ? pack_key(best, lin) : 0ull;
-            const unsigned long long wkey = warp_max_key(key);
-            const int wl = __ffs(__ballot_sync(0xffffffffu, key == wkey)) - 1;
-            if (lane == wl) {
+            const unsigned lin = bj >= 0 ? (unsigned)((u0 + RSTEP * bj) * F + v) : 0xFFFFFFFFu;
+            const unsigned long long key = ord_key(best);
+            unsigned long long wkey;
+            unsigned wlin;
+            warp_argmax<T>(key, lin, wkey, wlin);
+            if (key == wkey && lin == wlin) {
                 sl[warp].key = wkey;
+                sl[warp].lin = wlin;
                 sl[warp].gre = bg.x;
                 sl[warp].gim = bg.y;
             }
         }
         __syncthreads();
-        const unsigned long long uk = lane < NW ? sl[lane].key : 0ull;
-        const unsigned long long gk = warp_max_key(uk);
-        const int gw = __ffs(__ballot_sync(0xffffffffu, uk == gk)) - 1;
-        int a, b;
+        int a, b, gw;
         if constexpr (IS_F32 && GUARD) {
+            const unsigned long long uk = lane < NW ? sl[lane].key : 0ull;
+            const unsigned long long gk = warp_max_key(uk);
+            gw = __ffs(__ballot_sync(0xffffffffu, uk == gk)) - 1;
             const int lin = (int)(0xFFFFFFFFu - (unsigned)(gk & 0xFFFFFFFFull));
             a = lin / F;
             b = lin - a * F;
@@ -452,18 +487,24 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
                 }
             }
         } else {
-            const int lin = 0xFFFF - (int)(gk & 0xFFFFull);
-            a = lin / F;
-            b = lin - a * F;
+            const unsigned long long uk = lane < NW ? sl[lane].key : 0ull;
+            const unsigned ul = lane < NW ? sl[lane].lin : 0xFFFFFFFFu;
+            unsigned long long gk;
+            unsigned glin;
+            warp_argmax<T>(uk, ul, gk, glin);
+            a = (int)(glin / F);
+            b = (int)(glin & (F - 1));
+            gw = (a % RSTEP) * SEG + (b >> 5);  // owner warp of bin (a, b)
         }
         // p = g[a,b] / sum(w) (_kernel.pyx:46-47); fp32 multiplies by 1/sum(w)
         T pre, pim;
+        const T2 gwin = *reinterpret_cast<const T2 *>(&sl[gw].gre);
         if constexpr (IS_F32) {
-            pre = sl[gw].gre * inv_tot;
-            pim = sl[gw].gim * inv_tot;
+            pre = gwin.x * inv_tot;
+            pim = gwin.y * inv_tot;
         } else {
-            pre = sl[gw].gre / tot;
-            pim = sl[gw].gim / tot;
+            pre = gwin.x / tot;
+            pim = gwin.y / tot;
         }
         const bool selfc = ((2 * a) & (F - 1)) == 0 && ((2 * b) & (F - 1)) == 0;
         if (t == 0 && picks_out) {
@@ -500,16 +541,32 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         k2 = 0;
         best = (T)-1;
         bj = -1;
+        // loads of a group of LG bins are issued before its math (smem latency)
+        constexpr int LG = IS_F32 ? 4 : 2;
 #pragma unroll
-        for (int j = 0; j < NB; ++j) {
-            const bool inr = (j < NB - 1) || (C::NSEGS % NW == 0) || (u0 + RSTEP * j < R1);
-            if (inr) {
-                G[j] = spectral_update(G[j], lo[j * RSTEP * F], hi[j * RSTEP * F], gpr, gpi);
-                const T e = G[j].x * G[j].x + G[j].y * G[j].y;
-                if (j == 0 || j == NB - 1) {
-                    if ((valid >> j) & 1u) track(j, e);
-                } else {
-                    track(j, e);
+        for (int j0 = 0; j0 < NB; j0 += LG) {
+            T2 wl[LG], wh[LG];
+#pragma unroll
+            for (int q = 0; q < LG; ++q) {
+                const int j = j0 + q;
+                const bool inr = j < NB && ((j < NB - 1) || (C::NSEGS % NW == 0) || (u0 + RSTEP * j < R1));
+                if (inr) {
+                    wl[q] = lo[j * RSTEP * F];
+                    wh[q] = hi[j * RSTEP * F];
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < LG; ++q) {
+                const int j = j0 + q;
+                const bool inr = j < NB && ((j < NB - 1) || (C::NSEGS % NW == 0) || (u0 + RSTEP * j < R1));
+                if (inr) {
+                    G[j] = spectral_update(G[j], wl[q], wh[q], gpr, gpi);
+                    const T e = G[j].x * G[j].x + G[j].y * G[j].y;
+                    if (j == 0 || j == NB - 1) {
+                        if ((valid >> j) & 1u) track(j, e);
+                    } else {
+                        track(j, e);
+                    }
                 }
             }
         }
