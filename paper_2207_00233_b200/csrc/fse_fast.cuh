@@ -62,7 +62,7 @@ struct FastSlot {
 };
 
 struct FastLayout {
-    size_t tw, slots, red, model, big, yx, yw, xs, ws, total;
+    size_t tw, slots, red, model, big, yx, yw, xs, ws, part, total;
 };
 
 template <typename T>
@@ -83,19 +83,22 @@ __host__ __device__ inline FastLayout fast_layout(int F, int NW, int Mmax, int N
     const size_t EXT = (size_t)(3 * F / 2 + 1) * F * c2;
     const size_t yb = (R1 * Nmax * c2 + 15) & ~size_t(15);
     const size_t xb = ((size_t)Mmax * Nmax * sizeof(T) + 15) & ~size_t(15);
-    // Yx / Yw / xs / ws must not overlap the W half-plane rows written by the
-    // fused row pass; everything is dead once the extension rows are filled.
-    if (yb <= HS) {
-        L.yx = 0;
-        L.yw = HE;
-    } else {
-        L.yx = HE;
-        L.yw = HE + yb;
-    }
-    L.xs = L.yw + yb;
+    const size_t pb = (R1 * (size_t)F * c2 + 15) & ~size_t(15);
+    // Phases (each separated by a barrier): column pass reads xs/ws, writes
+    // Yx/Yw; row partials read Yx (then Yw) and write part; the x combine reads
+    // part into registers, the w combine writes the W half rows [HS, HE) (Yx,
+    // Yw, xs, ws dead by then); the extension rows come last.
+    L.yx = 0;
+    L.yw = yb;
+    L.xs = 2 * yb;
     L.ws = L.xs + xb;
-    size_t bigb = L.ws + xb;
+    // partials live above the W half-plane rows [HS, HE), so the w-plane
+    // combine can store W rows directly
+    L.part = (2 * yb + 2 * xb > HE) ? 2 * yb + 2 * xb : HE;
+    size_t bigb = L.part + pb;
     if (bigb < EXT) bigb = EXT;
+    (void)HS;
+    (void)HE;
     L.total = L.big + bigb;
     return L;
 }
@@ -231,6 +234,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     T2 *Yw = reinterpret_cast<T2 *>(big + L.yw);
     T *xs = reinterpret_cast<T *>(big + L.xs);
     T *ws = reinterpret_cast<T *>(big + L.ws);
+    T2 *part = reinterpret_cast<T2 *>(big + L.part);
 
     // ---- window geometry (grid.py:108-135)
     int M, N, br0 = 0, bc0 = 0, bh = 0, bw = 0, wr0 = 0, wc0 = 0, frame = 0, blk = 0;
@@ -308,20 +312,35 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
 #pragma unroll
     for (int w = 0; w < NW; ++w) total += red[w];
 
-    // ---- DFT pass 1 (columns): Y[k1][n] = sum_m x[m][n] e^{-j 2 pi k1 m / F}, k1 <= F/2
-    for (int o = t; o < R1 * N; o += NT) {
+    // ---- DFT pass 1 (columns): Y[k1][n] = sum_m x[m][n] e^{-j 2 pi k1 m / F}, k1 <= F/2.
+    // x is real, so with even/odd partial sums Ee, Eo over m:
+    //   Y[k1] = Ee + Eo,  Y[F/2 - k1] = conj(Ee - Eo)    (e^{-j pi m} = (-1)^m)
+    // and only k1 <= F/4 is summed.
+    for (int o = t; o < (F / 4 + 1) * N; o += NT) {
         const int k1 = o / N, n = o - k1 * N;
-        T2 X = T2{0, 0}, Wc = T2{0, 0};
+        T2 Xe = T2{0, 0}, Xo = T2{0, 0}, We = T2{0, 0}, Wo = T2{0, 0};
         int k = 0;
-        for (int m = 0; m < M; ++m) {
+        for (int m = 0; m < M; m += 2) {
             const T2 tv = tw[k];
             const T xv = xs[m * N + n], wv = ws[m * N + n];
-            X = cfma(T2{xv, -xv}, tv, X);    // x e^{-j theta}
-            Wc = cfma(T2{wv, -wv}, tv, Wc);
+            Xe = cfma(T2{xv, -xv}, tv, Xe);  // x e^{-j theta}
+            We = cfma(T2{wv, -wv}, tv, We);
+            k = (k + k1) & (F - 1);
+            if (m + 1 < M) {
+                const T2 tu = tw[k];
+                const T xu = xs[(m + 1) * N + n], wu = ws[(m + 1) * N + n];
+                Xo = cfma(T2{xu, -xu}, tu, Xo);
+                Wo = cfma(T2{wu, -wu}, tu, Wo);
+            }
             k = (k + k1) & (F - 1);
         }
-        Yx[o] = X;
-        Yw[o] = Wc;
+        Yx[k1 * N + n] = cadd(Xe, Xo);
+        Yw[k1 * N + n] = cadd(We, Wo);
+        if (k1 != F / 4) {
+            const T2 dx = csub(Xe, Xo), dw = csub(We, Wo);
+            Yx[(F / 2 - k1) * N + n] = T2{dx.x, -dx.y};
+            Yw[(F / 2 - k1) * N + n] = T2{dw.x, -dw.y};
+        }
     }
     __syncthreads();
 
@@ -331,31 +350,66 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     const int u0 = warp / SEG;
     const int v = seg * 32 + lane;
 
-    // ---- DFT pass 2 (rows), fused for x and w: g (canonical bins) into
-    // registers, W half-plane rows into ext rows F/2 .. F.
+    // ---- DFT pass 2 (rows), radix-4 over the owners of columns v0 + q F/4:
+    //   P_r = sum_{n = r mod 4} Y[u][n] e^{-j 2 pi v0 n / F},
+    //   G[u][v0 + q F/4] = sum_r (-j)^{q r} P_r.
+    // The owner of quarter q computes P_q (N/4 terms) into `part`, then every
+    // owner combines the four partials of its bins.  g is kept for canonical
+    // bins; W goes to registers first, to the ext rows once `part` is dead.
+    constexpr int QW = F / 4;
+    const int q4 = v / QW, v0 = v - q4 * QW;
+    auto partials = [&](const T2 *Y) {
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+            const int u = u0 + RSTEP * j;
+            if (u < R1) {
+                const T2 *yr = Y + u * N;
+                T2 acc = T2{0, 0};
+                int k = (v0 * q4) & (F - 1);
+                const int step = (4 * v0) & (F - 1);
+                for (int n = q4; n < N; n += 4) {
+                    acc = dft_mac(acc, yr[n], tw[k]);
+                    k = (k + step) & (F - 1);
+                }
+                part[(u * 4 + q4) * QW + v0] = acc;
+            }
+        }
+    };
+    auto combine = [&](int u) -> T2 {
+        const T2 *pr = part + (u * 4) * QW + v0;
+        T2 acc = pr[0];
+#pragma unroll
+        for (int r = 1; r < 4; ++r) {
+            const T2 pv = pr[r * QW];
+            switch ((q4 * r) & 3) {  // (-j)^{q r}
+                case 0: acc = cadd(acc, pv); break;
+                case 1: acc = cadd(acc, T2{pv.y, -pv.x}); break;
+                case 2: acc = csub(acc, pv); break;
+                default: acc = cadd(acc, T2{-pv.y, pv.x}); break;
+            }
+        }
+        return acc;
+    };
     T2 G[NB];
     unsigned valid = 0;  // bit j: bin j is a canonical in-range bin
+    partials(Yx);
+    __syncthreads();
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
         const int u = u0 + RSTEP * j;
         G[j] = T2{0, 0};
-        if (u < R1) {
-            const T2 *yx = Yx + u * N, *yw = Yw + u * N;
-            T2 ga = T2{0, 0}, wa = T2{0, 0};
-            int k = 0;
-            for (int n = 0; n < N; ++n) {
-                const T2 tv = tw[k];
-                ga = dft_mac(ga, yx[n], tv);
-                wa = dft_mac(wa, yw[n], tv);
-                k = (k + v) & (F - 1);
-            }
-            Wext[(u + F / 2) * F + v] = wa;
-            const bool canon = !((u == 0 || u == F / 2) && v > F / 2);
-            if (canon) {
-                G[j] = ga;
-                valid |= 1u << j;
-            }
+        if (u < R1 && !((u == 0 || u == F / 2) && v > F / 2)) {
+            G[j] = combine(u);
+            valid |= 1u << j;
         }
+    }
+    __syncthreads();
+    partials(Yw);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+        const int u = u0 + RSTEP * j;
+        if (u < R1) Wext[(u + F / 2) * F + v] = combine(u);
     }
     __syncthreads();
     // extension rows: W[-s] = conj W[s] reflected, W[F] = W[0]
