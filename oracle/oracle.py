@@ -283,6 +283,8 @@ class Report:
     batches: list = field(default_factory=list)
     unconcealed_blocks: list = field(default_factory=list)
     picks: dict = field(default_factory=dict)
+    sched_time: float = 0.0   # seconds spent in schedule_all (inside wall_time)
+    n_lossy: int = 0          # lossy blocks of the whole frame
 
 
 def conceal(image, mask, p: Params, order="optimized", kernel="auto", want_picks=False,
@@ -299,6 +301,7 @@ def conceal(image, mask, p: Params, order="optimized", kernel="auto", want_picks
     table = lost_per_block(grid, msk)
     t0 = time.perf_counter()
     picks_out = {}
+    sched_time = 0.0
     batches, deferred = [], []
     processed = 0
 
@@ -332,7 +335,10 @@ def conceal(image, mask, p: Params, order="optimized", kernel="auto", want_picks
             if block_limit and processed >= block_limit:
                 break
     else:
-        for phase in schedule_all(grid, init_counts(grid, table)):
+        ts = time.perf_counter()
+        phases = schedule_all(grid, init_counts(grid, table))
+        sched_time = time.perf_counter() - ts
+        for phase in phases:
             snaps = [snap(b) for b in phase]
             done = []
             for b, s in zip(phase, snaps):
@@ -364,5 +370,6 @@ def conceal(image, mask, p: Params, order="optimized", kernel="auto", want_picks
         if len(still) == len(pending):
             break
         pending = still
-    rep = Report(order, processed, time.perf_counter() - t0, batches, pending, picks_out)
+    rep = Report(order, processed, time.perf_counter() - t0, batches, pending, picks_out,
+                 sched_time, int((table > 0).sum()))
     return img, msk, rep

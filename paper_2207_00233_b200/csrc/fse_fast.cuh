@@ -61,12 +61,20 @@ struct FastSlot {
     T gre, gim;              // g of the warp's best bin
 };
 
+// One iteration's contribution to the block model: pick (a, b) and gamma*p.
+template <typename T>
+struct PickRec {
+    int a, b;
+    T gpr, gpi;
+};
+
 struct FastLayout {
-    size_t tw, slots, red, model, big, yx, yw, xs, ws, part, total;
+    size_t tw, slots, red, model, hist, big, yx, yw, xs, ws, part, total;
 };
 
 template <typename T>
-__host__ __device__ inline FastLayout fast_layout(int F, int NW, int Mmax, int Nmax, int model_n) {
+__host__ __device__ inline FastLayout fast_layout(int F, int NW, int Mmax, int Nmax, int model_n,
+                                                  int iters) {
     FastLayout L;
     const size_t c2 = 2 * sizeof(T);
     size_t o = 0;
@@ -75,6 +83,8 @@ __host__ __device__ inline FastLayout fast_layout(int F, int NW, int Mmax, int N
     L.slots = o; o += 2 * (size_t)NW * sizeof(FastSlot<double>);
     L.red = o; o += (size_t)(NW + 2) * sizeof(double);
     L.model = o; o += (size_t)(model_n > 0 ? model_n : 1) * sizeof(T);
+    o = (o + 15) & ~size_t(15);
+    L.hist = o; o += (size_t)(model_n > 0 ? (iters > 0 ? iters : 1) : 1) * sizeof(PickRec<T>);
     o = (o + 127) & ~size_t(127);
     L.big = o;
     const size_t R1 = F / 2 + 1;
@@ -235,6 +245,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     T *xs = reinterpret_cast<T *>(big + L.xs);
     T *ws = reinterpret_cast<T *>(big + L.ws);
     T2 *part = reinterpret_cast<T2 *>(big + L.part);
+    PickRec<T> *hist = reinterpret_cast<PickRec<T> *>(sm + L.hist);
 
     // ---- window geometry (grid.py:108-135)
     int M, N, br0 = 0, bc0 = 0, bh = 0, bw = 0, wr0 = 0, wc0 = 0, frame = 0, blk = 0;
@@ -576,14 +587,9 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
             gpi = (T)0;
         }
 
-        // ---- (2) model over the block: 2 Re(gp e^{+j 2 pi (a i + b j)/F}) (fse.py:159)
+        // ---- (2) log the pick for the block model (synthesised after the loop)
         if constexpr (MODE == 0) {
-#pragma unroll
-            for (int k = 0; k < 2; ++k)
-                if (mown[k]) {
-                    const T2 ph = tw[(a * mi[k] + b * mj[k]) & (F - 1)];
-                    mval[k] += (T)2 * (gpr * ph.x - gpi * ph.y);
-                }
+            if (t == 0) hist[it] = PickRec<T>{a, b, gpr, gpi};
         }
         if (it + 1 == I) break;  // the last spectrum update is never observed
 
@@ -624,6 +630,20 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
                 }
             }
         }
+    }
+
+    // ---- model over the block: sum_it 2 Re(gamma p_it e^{+j 2 pi (a i + b j)/F}),
+    // fse.py:159 restricted to the block rect, accumulated in iteration order
+    if constexpr (MODE == 0) {
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+            if (mown[k])
+                for (int it = 0; it < I; ++it) {
+                    const PickRec<T> h = hist[it];
+                    const T2 ph = tw[(h.a * mi[k] + h.b * mj[k]) & (F - 1)];
+                    mval[k] += (T)2 * (h.gpr * ph.x - h.gpi * ph.y);
+                }
     }
 
     // ---- write-back of the block's LOST samples (conceal.py:61-66)
