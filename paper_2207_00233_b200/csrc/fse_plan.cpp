@@ -21,6 +21,9 @@
 #include <climits>
 #include <cstring>
 #include <thread>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 #include "fse_common.h"
 
@@ -86,21 +89,27 @@ void schedule_impl(const int32_t *counts_in, int rows, int cols,
             maxc = std::max(maxc, (int)cnt[b]);
             ++pending;
         }
+    // bucket[c]: bitset of pending blocks with count c; summ[c]: bitset of its
+    // non-zero words, so a row-major scan skips empty stretches 64 words at a time
+    const int swords = (words + 63) / 64;
     std::vector<std::vector<uint64_t>> bucket(maxc + 1, std::vector<uint64_t>(words, 0));
+    std::vector<std::vector<uint64_t>> summ(maxc + 1, std::vector<uint64_t>(swords, 0));
     std::vector<long> bsize(maxc + 1, 0);
-    std::vector<int> lo_word(maxc + 1, 0);  // no set bit below this word
     for (int b = 0; b < nb; ++b)
         if (cnt[b] >= 0) {
             bucket[cnt[b]][b >> 6] |= 1ull << (b & 63);
+            summ[cnt[b]][b >> 12] |= 1ull << ((b >> 6) & 63);
             ++bsize[cnt[b]];
         }
     auto add = [&](int c, int b) {
         bucket[c][b >> 6] |= 1ull << (b & 63);
+        summ[c][b >> 12] |= 1ull << ((b >> 6) & 63);
         ++bsize[c];
-        lo_word[c] = std::min(lo_word[c], b >> 6);
     };
     auto del = [&](int c, int b) {
-        bucket[c][b >> 6] &= ~(1ull << (b & 63));
+        uint64_t &w = bucket[c][b >> 6];
+        w &= ~(1ull << (b & 63));
+        if (!w) summ[c][b >> 12] &= ~(1ull << ((b >> 6) & 63));
         --bsize[c];
     };
     std::vector<int32_t> taken(nb, -1);
@@ -114,27 +123,30 @@ void schedule_impl(const int32_t *counts_in, int rows, int cols,
         while (bsize[nmin] == 0) ++nmin;
         batch.clear();
         auto &bits = bucket[nmin];
-        int w0 = lo_word[nmin];
-        while (w0 < words && bits[w0] == 0) ++w0;
-        lo_word[nmin] = w0;
-        for (int w = w0; w < words; ++w) {
-            uint64_t m = bits[w];
-            while (m) {
-                int b = (w << 6) + __builtin_ctzll(m);
-                m &= m - 1;
-                int r = b / cols, c = b - r * cols;
-                // only row-major-earlier neighbours can already be taken
-                bool clash = false;
-                if (c > 0 && taken[b - 1] == phase) clash = true;
-                if (!clash && r > 0) {
-                    int up = b - cols;
-                    if (taken[up] == phase || (c > 0 && taken[up - 1] == phase) ||
-                        (c + 1 < cols && taken[up + 1] == phase))
-                        clash = true;
+        auto &sum = summ[nmin];
+        for (int sw = 0; sw < swords; ++sw) {
+            uint64_t sm = sum[sw];
+            while (sm) {
+                const int w = (sw << 6) + __builtin_ctzll(sm);
+                sm &= sm - 1;
+                uint64_t m = bits[w];
+                while (m) {
+                    int b = (w << 6) + __builtin_ctzll(m);
+                    m &= m - 1;
+                    int r = b / cols, c = b - r * cols;
+                    // only row-major-earlier neighbours can already be taken
+                    bool clash = false;
+                    if (c > 0 && taken[b - 1] == phase) clash = true;
+                    if (!clash && r > 0) {
+                        int up = b - cols;
+                        if (taken[up] == phase || (c > 0 && taken[up - 1] == phase) ||
+                            (c + 1 < cols && taken[up + 1] == phase))
+                            clash = true;
+                    }
+                    if (clash) continue;
+                    taken[b] = phase;
+                    batch.push_back(b);
                 }
-                if (clash) continue;
-                taken[b] = phase;
-                batch.push_back(b);
             }
         }
         for (int b : batch) {
@@ -194,17 +206,31 @@ int build_one(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p, in
     P.iterations = p->iterations; P.fft1 = p->fft1; P.fft2 = p->fft2;
     P.rho = p->rho; P.delta = p->delta; P.gamma = p->gamma;
 
+    const bool prof = getenv("FSE_PLAN_TIMING") != nullptr;
+    auto clk = [] { return std::chrono::steady_clock::now(); };
+    auto t_start = clk();
+    auto lap = [&](const char *what) {
+        if (!prof) return;
+        auto now = clk();
+        fprintf(stderr, "plan %-12s %.1f ms\n", what, std::chrono::duration<double, std::milli>(now - t_start).count());
+        t_start = now;
+    };
     // per-block tallies: lost (grid.py:138-144), usable-as-A, pre-reconstructed
     std::vector<int32_t> nL(nb, 0), nA(nb, 0), nR0(nb, 0);
     for (int y = 0; y < H; ++y) {
         const uint8_t *row = mask + (size_t)y * W;
         int32_t *L = &nL[(y / B) * cols], *A = &nA[(y / B) * cols], *R0 = &nR0[(y / B) * cols];
-        for (int x = 0; x < W; ++x) {
-            uint8_t s = row[x];
-            int c = x / B;
-            if (s == FSE_LOST) ++L[c];
-            else if (s == FSE_RECONSTRUCTED) ++R0[c];
-            else ++A[c];  // anything else classifies as A (grid.py:124-130)
+        for (int c = 0; c < cols; ++c) {
+            const int x1 = std::min(W, (c + 1) * B);
+            int32_t l = 0, r0 = 0;
+            for (int x = c * B; x < x1; ++x) {
+                const uint8_t s = row[x];
+                l += s == FSE_LOST;
+                r0 += s == FSE_RECONSTRUCTED;
+            }
+            L[c] += l;
+            R0[c] += r0;
+            A[c] += (x1 - c * B) - l - r0;  // anything else classifies as A (grid.py:124-130)
         }
     }
     std::vector<uint8_t> lossy(nb);
@@ -216,6 +242,7 @@ int build_one(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p, in
     P.max_wr = std::min(H, B + 2 * p->d);
     P.max_wc = std::min(W, B + 2 * p->d);
 
+    lap("tallies");
     // processing phases in reference order
     std::vector<int32_t> ph_ptr, ph_blocks;
     if (order == FSE_ORDER_OPTIMIZED) {
@@ -231,11 +258,35 @@ int build_one(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p, in
             }
     }
 
+    lap("schedule");
     // degeneracy (fse.py:150-151): no sample of positive weight.  A samples
     // always weigh rho^dist > 0; R samples weigh delta*rho^dist, > 0 iff delta > 0.
     std::vector<uint8_t> written(nb, 0);
     const bool r_counts = p->delta > 0.0;
+    // Fast path: a block lying wholly inside the window that holds an A sample
+    // (or, with delta > 0, a pre-reconstructed sample) makes the window usable
+    // whatever was written since; count such blocks with a 2-D prefix sum.
+    std::vector<int32_t> PS((size_t)(rows + 1) * (cols + 1), 0);
+    for (int r = 0; r < rows; ++r)
+        for (int c = 0; c < cols; ++c) {
+            const int o = r * cols + c;
+            const int ok = nA[o] > 0 || (r_counts && nR0[o] > 0);
+            PS[(size_t)(r + 1) * (cols + 1) + c + 1] = ok + PS[(size_t)r * (cols + 1) + c + 1] +
+                                                       PS[(size_t)(r + 1) * (cols + 1) + c] -
+                                                       PS[(size_t)r * (cols + 1) + c];
+        }
+    auto static_usable = [&](int b) -> bool {
+        int wr0, wr1, wc0, wc1;
+        G.window_rect(b, wr0, wr1, wc0, wc1);
+        const int ilo = (wr0 + B - 1) / B, ihi = wr1 == H ? rows - 1 : wr1 / B - 1;
+        const int jlo = (wc0 + B - 1) / B, jhi = wc1 == W ? cols - 1 : wc1 / B - 1;
+        if (ilo > ihi || jlo > jhi) return false;
+        const size_t C1 = cols + 1;
+        return PS[(ihi + 1) * C1 + jhi + 1] - PS[ilo * C1 + jhi + 1] - PS[(ihi + 1) * C1 + jlo] +
+                   PS[ilo * C1 + jlo] > 0;
+    };
     auto usable = [&](int b) -> bool {
+        if (static_usable(b)) return true;
         int wr0, wr1, wc0, wc1;
         G.window_rect(b, wr0, wr1, wc0, wc1);
         int br0 = wr0 / B, br1 = (wr1 - 1) / B, bc0 = wc0 / B, bc1 = (wc1 - 1) / B;
@@ -310,22 +361,37 @@ int build_one(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p, in
     P.unconcealed = pending;
     P.n_processed = (int32_t)P.batch_blocks.size();
 
+    lap("ranks");
     // dependency levels over the processing order
     std::vector<int32_t> level(nb, -1);
+    // The window of block (r, c) covers exactly the blocks within Chebyshev
+    // radius R = ceil(d / B) (clamped to the grid): its rows run from
+    // floor((rB - d)/B) = r - ceil(d/B) to floor((rB + B + d - 1)/B) = r + ceil(d/B).
+    // level(b) = 1 + max level over lower-rank blocks in that square.  The square
+    // max is separable: HL[r][c] = max of level over row r, columns c +- R, kept
+    // up to date as batches are committed; a query is R*2+1 reads of HL.
+    const int R = (p->d + B - 1) / B;
+    std::vector<int32_t> HL(nb, -1);
     int n_levels = 0;
-    for (int b : P.batch_blocks) {
-        int wr0, wr1, wc0, wc1;
-        G.window_rect(b, wr0, wr1, wc0, wc1);
-        int br0 = wr0 / B, br1 = (wr1 - 1) / B, bc0 = wc0 / B, bc1 = (wc1 - 1) / B;
-        int lv = 0;
-        const int rb = P.rank[b];
-        for (int rr = br0; rr <= br1; ++rr)
-            for (int cc = bc0; cc <= bc1; ++cc) {
-                int o = rr * cols + cc;
-                if (P.rank[o] < rb) lv = std::max(lv, level[o] + 1);
-            }
-        level[b] = lv;
-        n_levels = std::max(n_levels, lv + 1);
+    const int n_batches = (int)P.batch_ptr.size() - 1;
+    for (int k = 0; k < n_batches; ++k) {
+        const int i0 = P.batch_ptr[k], i1 = P.batch_ptr[k + 1];
+        for (int i = i0; i < i1; ++i) {  // a batch reads only earlier batches
+            const int b = P.batch_blocks[i];
+            const int r = b / cols, c = b - r * cols;
+            int m = -1;
+            for (int rr = std::max(0, r - R); rr <= std::min(rows - 1, r + R); ++rr)
+                m = std::max(m, HL[rr * cols + c]);
+            level[b] = m + 1;
+            n_levels = std::max(n_levels, m + 2);
+        }
+        for (int i = i0; i < i1; ++i) {
+            const int b = P.batch_blocks[i];
+            const int r = b / cols, c = b - r * cols;
+            int32_t *row = &HL[r * cols];
+            for (int cc = std::max(0, c - R); cc <= std::min(cols - 1, c + R); ++cc)
+                row[cc] = std::max(row[cc], level[b]);
+        }
     }
     P.level_ptr.assign(n_levels + 1, 0);
     for (int b : P.batch_blocks) ++P.level_ptr[level[b] + 1];
@@ -334,6 +400,7 @@ int build_one(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p, in
     std::vector<int32_t> fill(P.level_ptr.begin(), P.level_ptr.end() - 1);
     for (int b = 0; b < nb; ++b)  // row-major within a level
         if (level[b] >= 0) P.level_blocks[fill[level[b]]++] = b;
+    lap("levels");
     return FSE_OK;
 }
 
