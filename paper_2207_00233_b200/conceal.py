@@ -60,7 +60,10 @@ class Plan:
     def __del__(self):
         h = getattr(self, "handle", None)
         if h is not None and h.value:
-            _lib.lib().fse_plan_free(h)
+            try:
+                _lib.lib().fse_plan_free(h)
+            except Exception:  # interpreter shutdown: module globals already gone
+                pass
             self.handle = None
 
     def _csr(self, fn, n, m):
@@ -176,6 +179,29 @@ def run_frames_device(plans, images_dev, masks_dev, masks_out_dev, params: FsePa
         picks_dev.data_ptr() if picks_dev is not None else None, s))
 
 
+def plan_and_run(masks_host, images_dev, masks_dev, masks_out_dev, params: FseParams,
+                 precision: str, order: str = OPTIMIZED, plan_threads: int = 0,
+                 first_chunk: int | None = None) -> list:
+    """Plan n frames on host threads and run them on the device, overlapping the
+    two: the first chunk (~1/8 of the frames) is planned and its level launches
+    queued, then the remaining frames are planned while the GPU works on it.
+    Returns the plans (in frame order).  Device work is queued on the current
+    stream; nothing is synchronised."""
+    n = len(masks_host)
+    if n == 0:
+        return []
+    k0 = n if n < 4 else (first_chunk or max(1, -(-n // 8)))
+    plans = build_plans(masks_host[:k0], params, order, plan_threads)
+    run_frames_device(plans, images_dev[:k0], masks_dev[:k0],
+                      None if masks_out_dev is None else masks_out_dev[:k0], params, precision)
+    if k0 < n:
+        rest = build_plans(masks_host[k0:], params, order, plan_threads)
+        run_frames_device(rest, images_dev[k0:], masks_dev[k0:],
+                          None if masks_out_dev is None else masks_out_dev[k0:], params, precision)
+        plans += rest
+    return plans
+
+
 def _report(plan: Plan, order, threads, wall) -> ConcealReport:
     return ConcealReport(order=order, threads=threads, blocks_processed=plan.n_processed,
                          wall_time=wall, batches=plan.batches(),
@@ -242,11 +268,12 @@ def conceal_batch(images, masks, params: FseParams | None = None, order: str = O
     t0 = time.perf_counter()
     tdt = torch.float64 if precision == "fp64" else torch.float32
     # uploads are queued first (async from pinned memory); planning overlaps them
+    # and the device work of the first frames (plan_and_run)
     img_d = imgs.to(device="cuda", non_blocking=True).to(tdt)
     msk_d = msks.to(device="cuda", non_blocking=True)
-    plans = build_plans(list(msks.numpy()), params, order, plan_threads)
     out_d = torch.empty_like(msk_d)
-    run_frames_device(plans, list(img_d), list(msk_d), list(out_d), params, precision)
+    plans = plan_and_run(list(msks.numpy()), list(img_d), list(msk_d), list(out_d), params,
+                         precision, order, plan_threads)
     out_img = torch.empty(img_d.shape, dtype=tdt, pin_memory=True)
     out_msk = torch.empty(out_d.shape, dtype=torch.uint8, pin_memory=True)
     out_img.copy_(img_d, non_blocking=True)
