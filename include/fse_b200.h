@@ -151,6 +151,11 @@ int fse_conceal_frames(int32_t n, FsePlan *const *plans, void *const *images,
  * by the fp64 kernel before the next level.  tau0 < 0 disables the guard.
  * Default: off (tau0 = -1).  Process-wide. */
 int fse_set_guard(double tau0, double tau1);
+/* fse_conceal_frames execution mode for the fast path: 1 = one persistent
+ * dataflow launch (ready queue over per-block dependency counters; blocks start
+ * when their own inputs are written), 0 (default) = one launch per dependency
+ * level.  Results are identical.  Process-wide; FSE_DATAFLOW=1 sets the default. */
+int fse_set_dataflow(int32_t on);
 /* Windows redone in fp64 by the guard, summed over timed calls (fse_timing_*). */
 int64_t fse_guard_redo_count(int32_t reset);
 

@@ -21,7 +21,7 @@ EXPORTS = (
     "fse_plan_free", "fse_plan_sizes", "fse_plan_batches", "fse_plan_levels", "fse_plan_ranks",
     "fse_plan_unconcealed", "fse_init_counts", "fse_schedule_all", "fse_conceal_frames",
     "fse_launch_count", "fse_timing_enable", "fse_timing_read", "fse_fma_probe",
-    "fse_set_guard", "fse_guard_redo_count",
+    "fse_set_guard", "fse_guard_redo_count", "fse_set_dataflow",
 )
 
 
@@ -84,6 +84,7 @@ def lib():
         L.fse_fma_probe.argtypes = [_i32, _i32, _i32, _i32, _vp, _vp]
         L.fse_set_guard.argtypes = [ctypes.c_double, ctypes.c_double]
         L.fse_guard_redo_count.argtypes = [_i32]
+        L.fse_set_dataflow.argtypes = [_i32]
         L.fse_guard_redo_count.restype = ctypes.c_int64
         L.fse_launch_count.argtypes = [_i32]
         L.fse_launch_count.restype = ctypes.c_int64

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -28,6 +29,16 @@ static thread_local TimingState g_timing;
 // fp32 near-tie guard thresholds (fse_fast.cuh): redo in fp64 when
 // e1 - e2 <= (tau0 + tau1 * it) * e1.  Negative tau0 disables the guard.
 static double g_tau0 = -1.0, g_tau1 = 0.0;
+
+// Persistent dataflow launch instead of one launch per level.  Off by default:
+// measured on config 4 it ties the level launches (fp32) or loses 5% (fp64) —
+// the critical path is the DAG depth either way and the level launches already
+// keep ~97% wave efficiency.  FSE_DATAFLOW=1 or fse_set_dataflow(1) selects it.
+static bool g_dataflow = [] {
+    const char *e = getenv("FSE_DATAFLOW");
+    return e && e[0] == '1';
+}();
+bool dataflow_enabled() { return g_dataflow; }
 static long long g_redo_total = 0;
 
 // FP32 FMA throughput probe: 8 independent FFMA chains per thread.
@@ -180,6 +191,11 @@ int fse_set_guard(double tau0, double tau1) {
     return FSE_OK;
 }
 
+int fse_set_dataflow(int32_t on) {
+    fse::g_dataflow = on != 0;
+    return FSE_OK;
+}
+
 int64_t fse_guard_redo_count(int32_t reset) {
     const long long v = fse::g_redo_total;
     if (reset) fse::g_redo_total = 0;
@@ -217,7 +233,7 @@ int fse_run_windows(int32_t n, int32_t M, int32_t N, int32_t F1, int32_t F2, con
     a.picks = picks;
     cudaStream_t s = (cudaStream_t)stream;
     const bool dbg = energies != nullptr;
-    if (!dbg && F1 == F2 && fse::fast_supported(F1, M, N, 0)) {
+    if (!dbg && F1 == F2 && fse::fast_supported(dtype, F1, M, N, 0)) {
         fse::FastArgs f{};
         f.values = values;
         f.weights = weights;
@@ -274,13 +290,20 @@ int fse_conceal_frames(int32_t n, FsePlan *const *plans, void *const *images,
         }
     }
     lvl_off[n_levels] = (int)n_entries;
-    // one staging buffer: frame table | ranks | entries | redo list | redo counters
-    const size_t off_rank = ((sizeof(fse::FrameDesc) * n + 255) / 256) * 256;
-    const size_t off_ent = off_rank + ((sizeof(int32_t) * (size_t)nb * n + 255) / 256) * 256;
-    const size_t off_redo = off_ent + ((sizeof(int2) * std::max<size_t>(n_entries, 1) + 255) / 256) * 256;
-    const size_t off_cnt = off_redo + ((sizeof(int2) * std::max<size_t>(n_entries, 1) + 255) / 256) * 256;
-    const size_t bytes = off_cnt + sizeof(int) * std::max(n_levels, 1);
-    std::vector<unsigned char> host(bytes);
+    // one device staging buffer:
+    //   uploaded: frame table | ranks | entries (level order)
+    //   zeroed:   redo counters | work counter | completion flags
+    //   scratch:  redo list
+    auto up256 = [](size_t x) { return (x + 255) / 256 * 256; };
+    const size_t off_rank = up256(sizeof(fse::FrameDesc) * n);
+    const size_t off_ent = off_rank + up256(sizeof(int32_t) * (size_t)nb * n);
+    const size_t off_cnt = off_ent + up256(sizeof(int2) * std::max<size_t>(n_entries, 1));
+    const size_t off_next = off_cnt + up256(sizeof(int) * std::max(n_levels, 1));
+    const size_t off_done = off_next + 256;
+    const size_t off_queue = off_done + up256(sizeof(int) * (size_t)nb * n);
+    const size_t off_redo = off_queue + up256(sizeof(int) * std::max<size_t>(n_entries, 1));
+    const size_t bytes = off_redo + sizeof(int2) * std::max<size_t>(n_entries, 1);
+    std::vector<unsigned char> host(off_cnt);
     cudaStream_t s = (cudaStream_t)stream;
     unsigned char *dev = nullptr;
     FSE_CUDA_TRY(cudaMallocAsync((void **)&dev, bytes, s));
@@ -303,7 +326,10 @@ int fse_conceal_frames(int32_t n, FsePlan *const *plans, void *const *images,
                 for (int i = P.level_ptr[l]; i < P.level_ptr[l + 1]; ++i) ent[k++] = make_int2(f, P.level_blocks[i]);
             }
     }
-    cudaError_t ce = cudaMemcpyAsync(dev, host.data(), bytes, cudaMemcpyHostToDevice, s);
+    // pageable source: staged by the driver before returning, so `host` may go
+    cudaError_t ce = cudaMemcpyAsync(dev, host.data(), off_cnt, cudaMemcpyHostToDevice, s);
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(dev + off_cnt, 0, off_queue - off_cnt, s);
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(dev + off_queue, 0xFF, off_redo - off_queue, s);
     if (ce != cudaSuccess) {
         cudaFreeAsync(dev, s);
         return fail(FSE_ECUDA, std::string("upload: ") + cudaGetErrorString(ce));
@@ -334,8 +360,9 @@ int fse_conceal_frames(int32_t n, FsePlan *const *plans, void *const *images,
         }
         cudaEventRecord(ev0, s);
     }
-    const bool fast = F1 == F2 && fse::fast_supported(F1, Mmax, Nmax, model_n);
-    const bool guard = fast && dtype == FSE_F32 && fse::g_tau0 >= 0.0;
+    const bool fast = F1 == F2 && fse::fast_supported(dtype, F1, Mmax, Nmax, model_n);
+    int n_levels_run = n_levels;
+    const bool guard = fast && dtype == FSE_F32 && fse::g_tau0 >= 0.0 && F1 != 128;
     fse::FastArgs f{};
     if (fast) {
         f.frames = a.frames;
@@ -356,7 +383,19 @@ int fse_conceal_frames(int32_t n, FsePlan *const *plans, void *const *images,
     }
     int2 *redo = reinterpret_cast<int2 *>(dev + off_redo);
     int *counters = reinterpret_cast<int *>(dev + off_cnt);
-    for (int l = 0; l < n_levels && rc == FSE_OK; ++l) {
+    if (fast && !guard && fse::dataflow_enabled()) {
+        // one persistent launch over all levels of all frames (fse_fast.cuh)
+        f.entries = reinterpret_cast<const int2 *>(dev + off_ent);
+        f.total = (int)n_entries;
+        f.next = reinterpret_cast<int *>(dev + off_next);
+        f.done = reinterpret_cast<int *>(dev + off_done);
+        f.queue = reinterpret_cast<int *>(dev + off_queue);
+        f.R = (P0.d + P0.B - 1) / P0.B;
+        if (n_entries > 0) rc = fse::fast_dataflow(dtype, F1, f, Mmax, Nmax, model_n, s);
+        if (fse::g_timing.on) ++fse::g_timing.window_launches;
+        n_levels_run = 0;
+    }
+    for (int l = 0; l < n_levels_run && rc == FSE_OK; ++l) {
         const int2 *lvl = reinterpret_cast<const int2 *>(dev + off_ent) + lvl_off[l];
         const int cnt = lvl_off[l + 1] - lvl_off[l];
         if (cnt == 0) continue;

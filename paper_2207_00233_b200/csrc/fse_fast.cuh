@@ -48,7 +48,7 @@ struct FastCfg {
     static constexpr int NB = (NSEGS + NW_ - 1) / NW_;  // segments (bins) per thread
     static constexpr int RSTEP = NW_ / SEG;     // row stride between a warp's segments
     static constexpr int EXT_ROWS = 3 * F_ / 2 + 1;
-    static_assert(F_ == 32 || F_ == 64, "fast path: F = 32 or 64");
+    static_assert(F_ == 32 || F_ == 64 || F_ == 128, "fast path: F = 32, 64 or 128");
     static_assert(NW_ % SEG == 0, "NW must be a multiple of F/32");
     static_assert(NB <= 32, "5-bit bin tag");
 };
@@ -136,6 +136,14 @@ struct FastArgs {
     float tau0, tau1;  // guard when e1 - e2 <= (tau0 + tau1 * it) * e1
     // persistent (redo) launch: entries[0 .. *count)
     const int *count;
+    // persistent dataflow launch (fse_fast_dataflow_kernel): entries[0 .. total)
+    // in dependency-level order, a work counter, one completion flag per
+    // (frame, block), and the dependency radius in blocks
+    int total;
+    int *next;   // [0] queue head, [1] queue tail
+    int *done;   // per (frame, block): outstanding dependency count
+    int *queue;  // ready queue, total slots, -1 = not yet written
+    int R;
 };
 
 __device__ __forceinline__ unsigned warp_max_u32(unsigned v) { return __reduce_max_sync(0xffffffffu, v); }
@@ -227,7 +235,7 @@ __device__ __forceinline__ T2 dft_mac(T2 acc, T2 z, T2 tw) {
 
 template <class C, int MODE, bool GUARD, typename IT>
 __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout &L, const int entry_idx,
-                                            unsigned char *sm) {
+                                            unsigned char *sm, int2 entry_in = make_int2(-1, -1)) {
     using T = typename C::T;
     using T2 = typename C::T2;
     constexpr int F = C::F, NW = C::NW, NT = C::NT, NB = C::NB, R1 = C::R1, SEG = C::SEG;
@@ -252,7 +260,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     const FrameDesc *fd = nullptr;
     int2 entry = make_int2(0, 0);
     if constexpr (MODE == 0) {
-        entry = A.entries[entry_idx];
+        entry = entry_in.x >= 0 ? entry_in : A.entries[entry_idx];
         frame = entry.x;
         blk = entry.y;
         fd = A.frames + frame;
@@ -676,10 +684,98 @@ __global__ void __launch_bounds__(C::NT) fse_fast_redo_kernel(const FastArgs A, 
     }
 }
 
-// Host launchers (fse_inst_fast.cu).  dtype FSE_F32/FSE_F64, F = 32/64.
-int fast_supported(int F, int Mmax, int Nmax, int model_n);
+// Persistent dataflow execution.  The level barrier is
+// replaced by per-block dependency counters over the rank-overlap DAG: block o
+// depends on every processed block of lower rank within the dependency radius
+// (its window reads their samples).  dataflow_init_kernel counts those
+// dependencies and enqueues the blocks that have none; the persistent kernel
+// pops ready blocks from a global queue, fits them, and on completion
+// decrements its dependents' counters, enqueueing each one whose count reaches
+// zero.  A CTA never holds a block that is not ready, so resident CTAs only wait
+// for the queue to grow, which the running CTAs guarantee: no deadlock.
+// Ordering: write-back -> bar.sync -> acq_rel counter decrement (release
+// sequence) -> st.release of the queue slot -> consumer ld.acquire.
+__device__ __forceinline__ int ld_acquire(const int *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int *p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int atom_add_acq_rel(int *p, int v) {
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
+// One thread per entry: dependency count; blocks without dependencies are queued.
+static __global__ void dataflow_init_kernel(const FastArgs A) {
+    const int nb = A.rows * A.cols;
+    const int R = A.R;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < A.total; e += gridDim.x * blockDim.x) {
+        const int2 en = A.entries[e];
+        const int *rank = A.frames[en.x].rank;
+        const int r = en.y / A.cols, c = en.y - r * A.cols;
+        const int myrank = rank[en.y];
+        int deps = 0;
+        for (int rr = max(0, r - R); rr <= min(A.rows - 1, r + R); ++rr)
+            for (int cc = max(0, c - R); cc <= min(A.cols - 1, c + R); ++cc)
+                deps += rank[rr * A.cols + cc] < myrank;
+        A.done[(size_t)en.x * nb + en.y] = deps;
+        if (deps == 0) {
+            const int k = atomicAdd(A.next + 1, 1);  // queue tail
+            A.queue[k] = en.x * nb + en.y;          // consumers start after this kernel
+        }
+    }
+}
+
+template <class C, typename IT>
+__global__ void __launch_bounds__(C::NT) fse_fast_dataflow_kernel(const FastArgs A, const FastLayout L) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    __shared__ int s_code;
+    const int t = threadIdx.x;
+    const int nb = A.rows * A.cols;
+    const int R = A.R, side = 2 * R + 1;
+    for (;;) {
+        if (t == 0) {
+            const int i = atomicAdd(A.next, 1);  // queue head
+            int code = -2;
+            if (i < A.total) {
+                while ((code = ld_acquire(A.queue + i)) < 0) __nanosleep(100);
+            }
+            s_code = code;
+        }
+        __syncthreads();
+        const int code = s_code;
+        if (code == -2) break;
+        const int2 en = make_int2(code / nb, code - (code / nb) * nb);
+        fast_window<C, 0, false, IT>(A, L, 0, sm, en);
+        __syncthreads();  // the CTA's write-back stores precede the releases below
+        const int *rank = A.frames[en.x].rank;
+        const int r = en.y / A.cols, c = en.y - r * A.cols;
+        const int myrank = rank[en.y];
+        int *cnt = A.done + (size_t)en.x * nb;
+        for (int q = t; q < side * side; q += C::NT) {
+            const int rr = r - R + q / side, cc = c - R + q % side;
+            if (rr < 0 || rr >= A.rows || cc < 0 || cc >= A.cols) continue;
+            const int o = rr * A.cols + cc;
+            const int ro = rank[o];
+            if (o == en.y || ro <= myrank || ro == 0x7FFFFFFF) continue;
+            if (atom_add_acq_rel(cnt + o, -1) == 1) {
+                const int k = atomicAdd(A.next + 1, 1);
+                st_release(A.queue + k, en.x * nb + o);
+            }
+        }
+    }
+}
+
+// Host launchers (fse_inst_fast.cu).  dtype FSE_F32/FSE_F64, F = 32/64 (and 128 in fp32).
+int fast_supported(int dtype, int F, int Mmax, int Nmax, int model_n);
 int fast_level(int dtype, int F, bool guard, const FastArgs &a, int grid, int Mmax, int Nmax,
                int model_n, cudaStream_t s);
+int fast_dataflow(int dtype, int F, const FastArgs &a, int Mmax, int Nmax, int model_n,
+                  cudaStream_t s);
 int fast_redo(int F, const FastArgs &a, int max_entries, int Mmax, int Nmax, int model_n,
               cudaStream_t s);
 int fast_windows(int dtype, int F, const FastArgs &a, int grid, cudaStream_t s);

@@ -1,5 +1,6 @@
 // Instantiation + host launchers of the fast-path kernel (fse_fast.cuh).
 #include <cstdlib>
+#include <algorithm>
 #include <string>
 
 #include "fse_fast.cuh"
@@ -12,10 +13,16 @@ namespace fse {
 template <typename T> using Fast64 = FastCfg<T, 64, 6>;
 
 template <typename T> using Fast32 = FastCfg<T, 32, 6>;
+// F = 128 (fp32 only: the row-extended W plane is 193 x 128 x 8 B = 198 KB):
+// 260 row segments over 20 warps -> 13 bins per thread, one CTA per SM.
+template <typename T> using Fast128 = FastCfg<T, 128, 20>;
+// (A 22-warp / 3-bin "latency" variant for levels narrower than the GPU was
+// measured 20% slower on configs 1-2: per-iteration overhead grows with warps.)
 
-int fast_supported(int F, int Mmax, int Nmax, int model_n) {
+int fast_supported(int dtype, int F, int Mmax, int Nmax, int model_n) {
     // model samples live in registers: at most 2 per thread
-    return (F == 32 || F == 64) && Mmax <= F && Nmax <= F && model_n <= 2 * 6 * 32;
+    const bool sizes = F == 32 || F == 64 || (F == 128 && dtype == FSE_F32);
+    return sizes && Mmax <= F && Nmax <= F && model_n <= 2 * 6 * 32;
 }
 
 template <class C, int MODE, bool GUARD>
@@ -63,9 +70,52 @@ static int launch_redo(const FastArgs &a, int max_entries, int Mmax, int Nmax, i
     return FSE_OK;
 }
 
+template <class C, typename IT>
+static int launch_dataflow(const FastArgs &a, int Mmax, int Nmax, int model_n, cudaStream_t s) {
+    const FastLayout L = fast_layout<typename C::T>(C::F, C::NW, Mmax, Nmax, model_n, a.iterations);
+    auto kern = fse_fast_dataflow_kernel<C, IT>;
+    static thread_local size_t configured = 0;
+    static thread_local int per_sm = 0, sms = 0;
+    if (L.total > configured) {
+        int dev = 0;
+        FSE_CUDA_TRY(cudaGetDevice(&dev));
+        FSE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
+        FSE_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::NT, L.total));
+        FSE_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        configured = L.total;
+    }
+    if (per_sm < 1) return fail(FSE_ENOTSUP, "dataflow kernel does not fit on an SM");
+    const int grid = std::max(1, std::min(a.total, per_sm * sms));
+    {
+        const int ib = 256, ig = std::max(1, std::min((a.total + ib - 1) / ib, sms * 8));
+        dataflow_init_kernel<<<ig, ib, 0, s>>>(a);
+        FSE_CUDA_TRY(cudaGetLastError());
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+    FastArgs args = a;
+    FastLayout lay = L;
+    void *params[] = {&args, &lay};
+    // cooperative launch: the whole grid is co-resident (the dependency waits
+    // rely on it)
+    FSE_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(C::NT), params, L.total, s));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return FSE_OK;
+}
+
+int fast_dataflow(int dtype, int F, const FastArgs &a, int Mmax, int Nmax, int model_n, cudaStream_t s) {
+    if (dtype == FSE_F32) {
+        if (F == 128) return launch_dataflow<Fast128<float>, float>(a, Mmax, Nmax, model_n, s);
+        if (F == 64) return launch_dataflow<Fast64<float>, float>(a, Mmax, Nmax, model_n, s);
+        return launch_dataflow<Fast32<float>, float>(a, Mmax, Nmax, model_n, s);
+    }
+    if (F == 64) return launch_dataflow<Fast64<double>, double>(a, Mmax, Nmax, model_n, s);
+    return launch_dataflow<Fast32<double>, double>(a, Mmax, Nmax, model_n, s);
+}
+
 int fast_level(int dtype, int F, bool guard, const FastArgs &a, int grid, int Mmax, int Nmax,
                int model_n, cudaStream_t s) {
     if (dtype == FSE_F32) {
+        if (F == 128) return launch<Fast128<float>, 0, false>(a, grid, Mmax, Nmax, model_n, s);
         if (F == 64)
             return guard ? launch<Fast64<float>, 0, true>(a, grid, Mmax, Nmax, model_n, s)
                          : launch<Fast64<float>, 0, false>(a, grid, Mmax, Nmax, model_n, s);
@@ -83,6 +133,7 @@ int fast_redo(int F, const FastArgs &a, int max_entries, int Mmax, int Nmax, int
 
 int fast_windows(int dtype, int F, const FastArgs &a, int grid, cudaStream_t s) {
     if (dtype == FSE_F32) {
+        if (F == 128) return launch<Fast128<float>, 1, false>(a, grid, a.M, a.N, 0, s);
         if (F == 64) return launch<Fast64<float>, 1, false>(a, grid, a.M, a.N, 0, s);
         return launch<Fast32<float>, 1, false>(a, grid, a.M, a.N, 0, s);
     }

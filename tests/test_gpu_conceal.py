@@ -246,3 +246,42 @@ def test_full_size_properties(config, prec, iters):
     truth = img.astype(np.float64)
     assert abs(psnr(truth, out, mask) - psnr(truth, out64, mask)) <= FP32_PSNR_DB
     assert np.mean(np.abs(out[lost] - out64[lost]) <= 0.5) >= 0.6
+
+
+@pytest.mark.parametrize("cfg,B,F,order", [(2, 4, 64, "optimized"), (2, 4, 64, "linescan"),
+                                           (5, 2, 32, "optimized")])
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_dataflow_equals_level_launches(cfg, B, F, order, prec):
+    """The persistent dataflow launch and the per-level launches compute the
+    same function (every block reads only lower-rank, completed blocks)."""
+    from paper_2207_00233_b200 import _lib
+
+    img, mask = synth.config_scene(cfg)
+    if cfg == 5:
+        img, mask = img[:256, :384].copy(), mask[:256, :384].copy()
+    p = P.FseParams(d=14, iterations=40, block_size=B, fft_size=F)
+    L = _lib.lib()
+    try:
+        L.fse_set_dataflow(1)
+        a, am, _ = P.conceal(img, mask, p, order, precision=prec)
+        L.fse_set_dataflow(0)
+        b, bm, _ = P.conceal(img, mask, p, order, precision=prec)
+    finally:
+        L.fse_set_dataflow(1)
+    assert a.tobytes() == b.tobytes()
+    np.testing.assert_array_equal(am, bm)
+
+
+@pytest.mark.parametrize("B,F", [(2, 32), (4, 64), (8, 128)])
+def test_config5_block_sizes_fp32_fast_path(B, F):
+    """fp32 fast kernels at F = 32 / 64 / 128 against the fp64 path on a crop of
+    BASELINE config 5 (statistical parity, FP32_PSNR_DB)."""
+    img, mask = synth.config_scene(5)
+    img, mask = img[:128, :192].copy(), mask[:128, :192].copy()
+    p = P.FseParams(d=14, iterations=60, block_size=B, fft_size=F)
+    o32, m32, _ = P.conceal(img, mask, p, precision="fp32")
+    o64, m64, _ = P.conceal(img, mask, p, precision="fp64")
+    np.testing.assert_array_equal(m32, m64)
+    truth = img.astype(np.float64)
+    assert abs(psnr(truth, o32, mask) - psnr(truth, o64, mask)) <= FP32_PSNR_DB
+    assert np.isfinite(o32).all()
