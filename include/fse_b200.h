@@ -159,6 +159,28 @@ int fse_set_dataflow(int32_t on);
 /* Windows redone in fp64 by the guard, summed over timed calls (fse_timing_*). */
 int64_t fse_guard_redo_count(int32_t reset);
 
+/* ------------------------------------------------------------------------
+ * Row-band shards of one frame (spatial strip sharding across GPUs, BASELINE
+ * config 5).  Every rank builds the same global plan
+ * (fse_plan_build is deterministic), opens a shard over its band of block rows
+ * [row_lo, row_hi) on its own device copy of the frame, and then alternates
+ * fse_shard_run over one level with a halo exchange: the image rows of the
+ * R = ceil(d/B) block rows at each band edge go to the neighbouring rank
+ * whenever that level wrote blocks there (edge_flags bit 0 = top zone,
+ * bit 1 = bottom zone).  Masks and ranks never change, so only image samples
+ * cross devices.  Same semantics as fse_conceal_frames on the whole frame.
+ * Replaces the batch loop of conceal() (conceal.py:145-163) for one band. */
+typedef struct FseShard FseShard;
+int fse_shard_open(const FsePlan *plan, int32_t row_lo, int32_t row_hi, void *image,
+                   const uint8_t *mask, uint8_t *mask_out, const FseParamsC *p, int32_t dtype,
+                   const void *decay, int32_t decay_dim, void *stream, FseShard **out);
+/* number of levels and, if edge_flags != NULL, int32[n_levels] edge flags */
+int fse_shard_levels(const FseShard *shard, int32_t *n_levels, int32_t *edge_flags);
+/* launch levels [level_lo, level_hi) of the band's blocks on stream */
+int fse_shard_run(FseShard *shard, int32_t level_lo, int32_t level_hi, void *stream);
+/* mask pass over the band's rows (if mask_out was given) and release */
+int fse_shard_close(FseShard *shard, void *stream);
+
 /* Count of kernel launches issued since the last reset (bench.py gpu_launches). */
 int64_t fse_launch_count(int32_t reset);
 

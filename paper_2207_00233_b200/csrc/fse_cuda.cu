@@ -85,13 +85,16 @@ __global__ void dfma_probe_kernel(float *out, int iters, double a, double b) {
 }
 
 // LOST samples of concealed blocks become RECONSTRUCTED (conceal.py:65-66)
-__global__ void finalize_masks_kernel(const FrameDesc *frames, int n, int H, int W, int B, int cols) {
-    const long long total = (long long)n * H * W;
+__global__ void finalize_masks_kernel(const FrameDesc *frames, int n, int H, int W, int B, int cols,
+                                      int y0, int y1) {
+    const int hh = y1 - y0;
+    const long long total = (long long)n * hh * W;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
-        const int f = (int)(i / ((long long)H * W));
-        const long long p = i - (long long)f * H * W;
-        const int y = (int)(p / W), x = (int)(p - (long long)y * W);
+        const int f = (int)(i / ((long long)hh * W));
+        const long long q = i - (long long)f * hh * W;
+        const int y = y0 + (int)(q / W), x = (int)(q - (long long)(q / W) * W);
+        const long long p = (long long)y * W + x;
         const FrameDesc &fd = frames[f];
         uint8_t s = fd.mask[p];
         if (s == FSE_LOST && fd.rank[(y / B) * cols + x / B] != INT_MAX) s = FSE_RECONSTRUCTED;
@@ -252,17 +255,39 @@ int fse_run_windows(int32_t n, int32_t M, int32_t N, int32_t F1, int32_t F2, con
                : fse::dispatch<float, 1, false>(a, n, M, N, F1, F2, 0, s);
 }
 
-int fse_conceal_frames(int32_t n, FsePlan *const *plans, void *const *images,
-                       const uint8_t *const *masks, uint8_t *const *masks_out,
-                       const FseParamsC *p, int32_t dtype, const void *decay, int32_t decay_dim,
-                       int32_t *picks, void *stream) {
-    if (n < 0 || (n > 0 && (!plans || !images || !masks || !p || !decay)))
-        return fail(FSE_EINVAL, "NULL argument");
-    if (n == 0) return FSE_OK;
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Device session: the staged plan(s) of one fse_conceal_frames call, or of one
+// row band of a frame (fse_shard_*).  open = upload ranks + level entry lists
+// (restricted to block rows [row_lo, row_hi)), run = launch levels [l0, l1),
+// close = mask pass over the band + free.
+
+struct FseShard {
+    int n = 0, H = 0, W = 0, B = 0, d = 0, rows = 0, cols = 0, nb = 0, R = 0;
+    int dtype = 0, F1 = 0, F2 = 0, Mmax = 0, Nmax = 0, model_n = 0;
+    int row_lo = 0, row_hi = 0, n_levels = 0;
+    size_t n_entries = 0;
+    std::vector<int> lvl_off;
+    std::vector<int32_t> edge;  // per level: bit0 top zone, bit1 bottom zone touched
+    unsigned char *dev = nullptr;
+    size_t off_ent = 0, off_cnt = 0, off_next = 0, off_done = 0, off_queue = 0, off_redo = 0;
+    bool fast = false, guard = false, masks_out = false;
+    fse::KArgs a{};
+    fse::FastArgs f{};
+};
+
+namespace fse {
+
+static int session_open(int32_t n, FsePlan *const *plans, void *const *images, const uint8_t *const *masks,
+                        uint8_t *const *masks_out, const FseParamsC *p, int32_t dtype, const void *decay,
+                        int32_t decay_dim, int32_t *picks, int row_lo, int row_hi, cudaStream_t s,
+                        FseShard **out) {
+    if (n < 1 || !plans || !images || !masks || !p || !decay || !out) return fail(FSE_EINVAL, "NULL argument");
     if (dtype != FSE_F64 && dtype != FSE_F32) return fail(FSE_EINVAL, "dtype");
-    const fse::Plan &P0 = plans[0]->p;
+    const Plan &P0 = plans[0]->p;
     for (int f = 0; f < n; ++f) {
-        const fse::Plan &P = plans[f]->p;
+        const Plan &P = plans[f]->p;
         if (!images[f] || !masks[f]) return fail(FSE_EINVAL, "NULL image/mask");
         if (P.H != P0.H || P.W != P0.W || P.B != P0.B || P.d != P0.d)
             return fail(FSE_EINVAL, "plans of one call must share image size, block size and d");
@@ -275,41 +300,68 @@ int fse_conceal_frames(int32_t n, FsePlan *const *plans, void *const *images,
         return fail(FSE_EINVAL, "FFT size smaller than the largest window");
     if (F1 && F1 > 0xFFFF / F2) return fail(FSE_EINVAL, "DFT too large");
     if (decay_dim < std::max(P0.max_wr, P0.max_wc)) return fail(FSE_EINVAL, "decay table too small");
+    row_lo = std::max(0, row_lo);
+    row_hi = std::min(P0.rows, row_hi);
+    if (row_lo >= row_hi) return fail(FSE_EINVAL, "empty block-row range");
 
-    const int nb = P0.rows * P0.cols;
+    FseShard *S = new FseShard();
+    S->n = n;
+    S->H = P0.H; S->W = P0.W; S->B = P0.B; S->d = P0.d; S->rows = P0.rows; S->cols = P0.cols;
+    S->nb = P0.rows * P0.cols;
+    S->R = (P0.d + P0.B - 1) / P0.B;
+    S->dtype = dtype; S->F1 = F1; S->F2 = F2;
+    S->Mmax = P0.max_wr; S->Nmax = P0.max_wc; S->model_n = P0.B * P0.B;
+    S->row_lo = row_lo; S->row_hi = row_hi;
+    S->masks_out = masks_out != nullptr;
+    const int nb = S->nb, cols = S->cols, R = S->R;
     int n_levels = 0;
     for (int f = 0; f < n; ++f) n_levels = std::max(n_levels, (int)plans[f]->p.level_ptr.size() - 1);
-    // merged level lists: level L of every frame in one launch
-    std::vector<int> lvl_off(n_levels + 1, 0);
+    S->n_levels = n_levels;
+    auto owned = [&](int b) { const int r = b / cols; return r >= row_lo && r < row_hi; };
+    // merged level lists: level L of every frame in one launch (owned rows only)
+    S->lvl_off.assign(n_levels + 1, 0);
+    S->edge.assign(n_levels, 0);
     size_t n_entries = 0;
     for (int l = 0; l < n_levels; ++l) {
-        lvl_off[l] = (int)n_entries;
+        S->lvl_off[l] = (int)n_entries;
         for (int f = 0; f < n; ++f) {
-            const fse::Plan &P = plans[f]->p;
-            if (l + 1 < (int)P.level_ptr.size()) n_entries += P.level_ptr[l + 1] - P.level_ptr[l];
+            const Plan &P = plans[f]->p;
+            if (l + 1 >= (int)P.level_ptr.size()) continue;
+            for (int i = P.level_ptr[l]; i < P.level_ptr[l + 1]; ++i) {
+                const int b = P.level_blocks[i];
+                if (!owned(b)) continue;
+                ++n_entries;
+                const int r = b / cols;
+                if (r < row_lo + R) S->edge[l] |= 1;
+                if (r >= row_hi - R) S->edge[l] |= 2;
+            }
         }
     }
-    lvl_off[n_levels] = (int)n_entries;
+    S->lvl_off[n_levels] = (int)n_entries;
+    S->n_entries = n_entries;
     // one device staging buffer:
     //   uploaded: frame table | ranks | entries (level order)
-    //   zeroed:   redo counters | work counter | completion flags
-    //   scratch:  redo list
+    //   zeroed:   redo counters | work/queue counters | dependency counters
+    //   scratch:  ready queue (0xFF) | redo list
     auto up256 = [](size_t x) { return (x + 255) / 256 * 256; };
-    const size_t off_rank = up256(sizeof(fse::FrameDesc) * n);
-    const size_t off_ent = off_rank + up256(sizeof(int32_t) * (size_t)nb * n);
-    const size_t off_cnt = off_ent + up256(sizeof(int2) * std::max<size_t>(n_entries, 1));
-    const size_t off_next = off_cnt + up256(sizeof(int) * std::max(n_levels, 1));
-    const size_t off_done = off_next + 256;
-    const size_t off_queue = off_done + up256(sizeof(int) * (size_t)nb * n);
-    const size_t off_redo = off_queue + up256(sizeof(int) * std::max<size_t>(n_entries, 1));
-    const size_t bytes = off_redo + sizeof(int2) * std::max<size_t>(n_entries, 1);
-    std::vector<unsigned char> host(off_cnt);
-    cudaStream_t s = (cudaStream_t)stream;
-    unsigned char *dev = nullptr;
-    FSE_CUDA_TRY(cudaMallocAsync((void **)&dev, bytes, s));
-    fse::FrameDesc *fdh = reinterpret_cast<fse::FrameDesc *>(host.data());
+    const size_t off_rank = up256(sizeof(FrameDesc) * n);
+    S->off_ent = off_rank + up256(sizeof(int32_t) * (size_t)nb * n);
+    S->off_cnt = S->off_ent + up256(sizeof(int2) * std::max<size_t>(n_entries, 1));
+    S->off_next = S->off_cnt + up256(sizeof(int) * std::max(n_levels, 1));
+    S->off_done = S->off_next + 256;
+    S->off_queue = S->off_done + up256(sizeof(int) * (size_t)nb * n);
+    S->off_redo = S->off_queue + up256(sizeof(int) * std::max<size_t>(n_entries, 1));
+    const size_t bytes = S->off_redo + sizeof(int2) * std::max<size_t>(n_entries, 1);
+    std::vector<unsigned char> host(S->off_cnt);
+    cudaError_t ce = cudaMallocAsync((void **)&S->dev, bytes, s);
+    if (ce != cudaSuccess) {
+        delete S;
+        return fail(FSE_ECUDA, std::string("staging alloc: ") + cudaGetErrorString(ce));
+    }
+    unsigned char *dev = S->dev;
+    FrameDesc *fdh = reinterpret_cast<FrameDesc *>(host.data());
     int32_t *rk = reinterpret_cast<int32_t *>(host.data() + off_rank);
-    int2 *ent = reinterpret_cast<int2 *>(host.data() + off_ent);
+    int2 *ent = reinterpret_cast<int2 *>(host.data() + S->off_ent);
     for (int f = 0; f < n; ++f) {
         fdh[f].image = images[f];
         fdh[f].mask = masks[f];
@@ -321,21 +373,23 @@ int fse_conceal_frames(int32_t n, FsePlan *const *plans, void *const *images,
         size_t k = 0;
         for (int l = 0; l < n_levels; ++l)
             for (int f = 0; f < n; ++f) {
-                const fse::Plan &P = plans[f]->p;
+                const Plan &P = plans[f]->p;
                 if (l + 1 >= (int)P.level_ptr.size()) continue;
-                for (int i = P.level_ptr[l]; i < P.level_ptr[l + 1]; ++i) ent[k++] = make_int2(f, P.level_blocks[i]);
+                for (int i = P.level_ptr[l]; i < P.level_ptr[l + 1]; ++i)
+                    if (owned(P.level_blocks[i])) ent[k++] = make_int2(f, P.level_blocks[i]);
             }
     }
     // pageable source: staged by the driver before returning, so `host` may go
-    cudaError_t ce = cudaMemcpyAsync(dev, host.data(), off_cnt, cudaMemcpyHostToDevice, s);
-    if (ce == cudaSuccess) ce = cudaMemsetAsync(dev + off_cnt, 0, off_queue - off_cnt, s);
-    if (ce == cudaSuccess) ce = cudaMemsetAsync(dev + off_queue, 0xFF, off_redo - off_queue, s);
+    ce = cudaMemcpyAsync(dev, host.data(), S->off_cnt, cudaMemcpyHostToDevice, s);
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(dev + S->off_cnt, 0, S->off_queue - S->off_cnt, s);
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(dev + S->off_queue, 0xFF, S->off_redo - S->off_queue, s);
     if (ce != cudaSuccess) {
         cudaFreeAsync(dev, s);
+        delete S;
         return fail(FSE_ECUDA, std::string("upload: ") + cudaGetErrorString(ce));
     }
-    fse::KArgs a{};
-    a.frames = reinterpret_cast<const fse::FrameDesc *>(dev);
+    KArgs &a = S->a;
+    a.frames = reinterpret_cast<const FrameDesc *>(dev);
     a.H = P0.H;
     a.W = P0.W;
     a.B = P0.B;
@@ -350,21 +404,10 @@ int fse_conceal_frames(int32_t n, FsePlan *const *plans, void *const *images,
     a.iterations = p->iterations;
     a.gamma = p->gamma;
     a.picks = picks;
-    const int Mmax = P0.max_wr, Nmax = P0.max_wc, model_n = P0.B * P0.B;
-    int rc = FSE_OK;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    if (fse::g_timing.on) {
-        if (cudaEventCreate(&ev0) != cudaSuccess || cudaEventCreate(&ev1) != cudaSuccess) {
-            cudaFreeAsync(dev, s);
-            return fail(FSE_ECUDA, "event create");
-        }
-        cudaEventRecord(ev0, s);
-    }
-    const bool fast = F1 == F2 && fse::fast_supported(dtype, F1, Mmax, Nmax, model_n);
-    int n_levels_run = n_levels;
-    const bool guard = fast && dtype == FSE_F32 && fse::g_tau0 >= 0.0 && F1 != 128;
-    fse::FastArgs f{};
-    if (fast) {
+    S->fast = F1 == F2 && fast_supported(dtype, F1, S->Mmax, S->Nmax, S->model_n);
+    S->guard = S->fast && dtype == FSE_F32 && g_tau0 >= 0.0 && F1 != 128;
+    if (S->fast) {
+        FastArgs &f = S->f;
         f.frames = a.frames;
         f.H = a.H;
         f.W = a.W;
@@ -378,66 +421,143 @@ int fse_conceal_frames(int32_t n, FsePlan *const *plans, void *const *images,
         f.iterations = a.iterations;
         f.gamma = a.gamma;
         f.picks = a.picks;
-        f.tau0 = (float)fse::g_tau0;
-        f.tau1 = (float)fse::g_tau1;
+        f.tau0 = (float)g_tau0;
+        f.tau1 = (float)g_tau1;
+        f.R = S->R;
     }
-    int2 *redo = reinterpret_cast<int2 *>(dev + off_redo);
-    int *counters = reinterpret_cast<int *>(dev + off_cnt);
-    if (fast && !guard && fse::dataflow_enabled()) {
+    *out = S;
+    return FSE_OK;
+}
+
+// Launch levels [l0, l1).  `whole` allows the dataflow executor (all levels at once).
+static int session_run(FseShard *S, int l0, int l1, bool whole, cudaStream_t s) {
+    l0 = std::max(0, l0);
+    l1 = std::min(S->n_levels, l1);
+    unsigned char *dev = S->dev;
+    int rc = FSE_OK;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (g_timing.on) {
+        if (cudaEventCreate(&ev0) != cudaSuccess || cudaEventCreate(&ev1) != cudaSuccess)
+            return fail(FSE_ECUDA, "event create");
+        cudaEventRecord(ev0, s);
+    }
+    int2 *redo = reinterpret_cast<int2 *>(dev + S->off_redo);
+    int *counters = reinterpret_cast<int *>(dev + S->off_cnt);
+    FastArgs &f = S->f;
+    KArgs &a = S->a;
+    if (whole && S->fast && !S->guard && dataflow_enabled()) {
         // one persistent launch over all levels of all frames (fse_fast.cuh)
-        f.entries = reinterpret_cast<const int2 *>(dev + off_ent);
-        f.total = (int)n_entries;
-        f.next = reinterpret_cast<int *>(dev + off_next);
-        f.done = reinterpret_cast<int *>(dev + off_done);
-        f.queue = reinterpret_cast<int *>(dev + off_queue);
-        f.R = (P0.d + P0.B - 1) / P0.B;
-        if (n_entries > 0) rc = fse::fast_dataflow(dtype, F1, f, Mmax, Nmax, model_n, s);
-        if (fse::g_timing.on) ++fse::g_timing.window_launches;
-        n_levels_run = 0;
+        f.entries = reinterpret_cast<const int2 *>(dev + S->off_ent);
+        f.total = (int)S->n_entries;
+        f.next = reinterpret_cast<int *>(dev + S->off_next);
+        f.done = reinterpret_cast<int *>(dev + S->off_done);
+        f.queue = reinterpret_cast<int *>(dev + S->off_queue);
+        if (S->n_entries > 0) rc = fast_dataflow(S->dtype, S->F1, f, S->Mmax, S->Nmax, S->model_n, s);
+        if (g_timing.on) ++g_timing.window_launches;
+        l1 = l0;
     }
-    for (int l = 0; l < n_levels_run && rc == FSE_OK; ++l) {
-        const int2 *lvl = reinterpret_cast<const int2 *>(dev + off_ent) + lvl_off[l];
-        const int cnt = lvl_off[l + 1] - lvl_off[l];
+    for (int l = l0; l < l1 && rc == FSE_OK; ++l) {
+        const int2 *lvl = reinterpret_cast<const int2 *>(dev + S->off_ent) + S->lvl_off[l];
+        const int cnt = S->lvl_off[l + 1] - S->lvl_off[l];
         if (cnt == 0) continue;
-        if (fast) {
+        if (S->fast) {
             f.entries = lvl;
-            f.redo_list = redo + lvl_off[l];
+            f.redo_list = redo + S->lvl_off[l];
             f.redo_count = counters + l;
-            rc = fse::fast_level(dtype, F1, guard, f, cnt, Mmax, Nmax, model_n, s);
-            if (rc == FSE_OK && guard) {
-                fse::FastArgs r = f;
-                r.entries = redo + lvl_off[l];
+            rc = fast_level(S->dtype, S->F1, S->guard, f, cnt, S->Mmax, S->Nmax, S->model_n, s);
+            if (rc == FSE_OK && S->guard) {
+                FastArgs r = f;
+                r.entries = redo + S->lvl_off[l];
                 r.count = counters + l;
-                rc = fse::fast_redo(F1, r, cnt, Mmax, Nmax, model_n, s);
+                rc = fast_redo(S->F1, r, cnt, S->Mmax, S->Nmax, S->model_n, s);
             }
         } else {
             a.entries = lvl;
-            rc = dtype == FSE_F64 ? fse::dispatch<double, 0, false>(a, cnt, Mmax, Nmax, F1, F2, model_n, s)
-                                  : fse::dispatch<float, 0, false>(a, cnt, Mmax, Nmax, F1, F2, model_n, s);
+            rc = S->dtype == FSE_F64
+                     ? dispatch<double, 0, false>(a, cnt, S->Mmax, S->Nmax, S->F1, S->F2, S->model_n, s)
+                     : dispatch<float, 0, false>(a, cnt, S->Mmax, S->Nmax, S->F1, S->F2, S->model_n, s);
         }
-        if (fse::g_timing.on) ++fse::g_timing.window_launches;
+        if (g_timing.on) ++g_timing.window_launches;
     }
-    if (fse::g_timing.on && guard && n_levels > 0) {
+    if (g_timing.on && S->guard && l1 > l0) {
         int *hc = nullptr;
-        if (cudaMallocHost((void **)&hc, sizeof(int) * n_levels) == cudaSuccess) {
-            cudaMemcpyAsync(hc, counters, sizeof(int) * n_levels, cudaMemcpyDeviceToHost, s);
-            fse::g_timing.redo.emplace_back(hc, n_levels);
+        if (cudaMallocHost((void **)&hc, sizeof(int) * (l1 - l0)) == cudaSuccess) {
+            cudaMemcpyAsync(hc, counters + l0, sizeof(int) * (l1 - l0), cudaMemcpyDeviceToHost, s);
+            g_timing.redo.emplace_back(hc, l1 - l0);
         }
     }
-    if (fse::g_timing.on) {
+    if (g_timing.on) {
         cudaEventRecord(ev1, s);
-        fse::g_timing.ev.emplace_back(ev0, ev1);
+        g_timing.ev.emplace_back(ev0, ev1);
     }
-    if (rc == FSE_OK && masks_out) {
-        const long long total = (long long)n * P0.H * P0.W;
-        int grid = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
-        fse::finalize_masks_kernel<<<grid, 256, 0, s>>>(a.frames, n, P0.H, P0.W, P0.B, P0.cols);
-        ce = cudaGetLastError();
-        if (ce != cudaSuccess) rc = fail(FSE_ECUDA, std::string("finalize: ") + cudaGetErrorString(ce));
-        else fse::g_launches.fetch_add(1, std::memory_order_relaxed);
-    }
-    cudaFreeAsync(dev, s);
     return rc;
+}
+
+static int session_close(FseShard *S, bool finalize, cudaStream_t s) {
+    int rc = FSE_OK;
+    if (finalize && S->masks_out) {
+        const int y0 = S->row_lo * S->B, y1 = std::min(S->H, S->row_hi * S->B);
+        const long long total = (long long)S->n * (y1 - y0) * S->W;
+        int grid = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+        if (grid > 0) {
+            finalize_masks_kernel<<<grid, 256, 0, s>>>(S->a.frames, S->n, S->H, S->W, S->B, S->cols, y0, y1);
+            cudaError_t ce = cudaGetLastError();
+            if (ce != cudaSuccess) rc = fail(FSE_ECUDA, std::string("finalize: ") + cudaGetErrorString(ce));
+            else g_launches.fetch_add(1, std::memory_order_relaxed);
+        }
+    }
+    cudaFreeAsync(S->dev, s);
+    delete S;
+    return rc;
+}
+
+}  // namespace fse
+
+extern "C" {
+
+int fse_conceal_frames(int32_t n, FsePlan *const *plans, void *const *images,
+                       const uint8_t *const *masks, uint8_t *const *masks_out,
+                       const FseParamsC *p, int32_t dtype, const void *decay, int32_t decay_dim,
+                       int32_t *picks, void *stream) {
+    if (n < 0) return fail(FSE_EINVAL, "n < 0");
+    if (n == 0) return FSE_OK;
+    if (!plans || !plans[0]) return fail(FSE_EINVAL, "NULL plan");
+    cudaStream_t s = (cudaStream_t)stream;
+    FseShard *S = nullptr;
+    int rc = fse::session_open(n, plans, images, masks, masks_out, p, dtype, decay, decay_dim, picks, 0,
+                               plans[0]->p.rows, s, &S);
+    if (rc) return rc;
+    rc = fse::session_run(S, 0, S->n_levels, true, s);
+    const int rc2 = fse::session_close(S, rc == FSE_OK, s);
+    return rc ? rc : rc2;
+}
+
+int fse_shard_open(const FsePlan *plan, int32_t row_lo, int32_t row_hi, void *image, const uint8_t *mask,
+                   uint8_t *mask_out, const FseParamsC *p, int32_t dtype, const void *decay,
+                   int32_t decay_dim, void *stream, FseShard **out) {
+    if (!plan) return fail(FSE_EINVAL, "NULL plan");
+    FsePlan *pl = const_cast<FsePlan *>(plan);
+    void *im = image;
+    uint8_t *mo = mask_out;
+    return fse::session_open(1, &pl, &im, &mask, mask_out ? &mo : nullptr, p, dtype, decay, decay_dim,
+                             nullptr, row_lo, row_hi, (cudaStream_t)stream, out);
+}
+
+int fse_shard_levels(const FseShard *sh, int32_t *n_levels, int32_t *edge_flags) {
+    if (!sh || !n_levels) return fail(FSE_EINVAL, "NULL argument");
+    *n_levels = sh->n_levels;
+    if (edge_flags) std::copy(sh->edge.begin(), sh->edge.end(), edge_flags);
+    return FSE_OK;
+}
+
+int fse_shard_run(FseShard *sh, int32_t level_lo, int32_t level_hi, void *stream) {
+    if (!sh) return fail(FSE_EINVAL, "NULL shard");
+    return fse::session_run(sh, level_lo, level_hi, false, (cudaStream_t)stream);
+}
+
+int fse_shard_close(FseShard *sh, void *stream) {
+    if (!sh) return fail(FSE_EINVAL, "NULL shard");
+    return fse::session_close(sh, true, (cudaStream_t)stream);
 }
 
 }  // extern "C"

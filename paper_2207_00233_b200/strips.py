@@ -1,0 +1,190 @@
+"""Spatial strip sharding of one large frame across GPUs (BASELINE config 5).
+
+One process per GPU; every rank builds the same global plan (the C++ planner
+is deterministic), so ranks, batches and dependency levels agree everywhere.
+Rank r owns a band of block rows [lo_r, hi_r), balanced by lossy-block count.
+Level by level, each rank fits the blocks of its band and then swaps halos with
+its neighbours: the window of a block reaches R = ceil(d/B) block rows, so the
+image rows of the R block rows at a band edge are sent to the neighbouring rank
+whenever that level wrote blocks there.  Masks and ranks never change (the
+snapshot semantics is rank-based), so only image samples move.
+The reference has no counterpart: its only parallelism is a thread pool over
+one batch (fsefill/conceal.py:146-153).
+
+The level loop and the exchange schedule are written against a small executor
+interface so the same protocol runs on GPUs (ShardExecutor, C ABI fse_shard_*,
+NCCL point-to-point) and, in tests, on CPU ranks over gloo with an emulated
+kernel.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .conceal import DeviceContext, build_plan
+from .fse import FseParams
+
+
+def halo_rows(params: FseParams) -> int:
+    """Dependency radius in block rows: a window spans block +- d samples."""
+    return -(-params.d // params.block_size) if params.d > 0 else 0
+
+
+def band_partition(lossy_per_row, world: int, R: int) -> list:
+    """Split block rows into `world` contiguous bands with about equal lossy-block
+    counts; every band keeps at least max(R, 1) rows so halos come only from the
+    adjacent ranks."""
+    rows = len(lossy_per_row)
+    min_rows = max(R, 1)
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    if world * min_rows > rows:
+        raise ValueError(f"{rows} block rows cannot be split into {world} bands of >= {min_rows} rows")
+    w = np.asarray(lossy_per_row, dtype=np.float64) + 1e-3  # empty rows still cost a little
+    cum = np.concatenate([[0.0], np.cumsum(w)])
+    cuts = [0]
+    for k in range(1, world):
+        target = cum[-1] * k / world
+        c = int(np.searchsorted(cum, target))
+        lo_ok = cuts[-1] + min_rows
+        hi_ok = rows - (world - k) * min_rows
+        cuts.append(min(max(c, lo_ok), hi_ok))
+    cuts.append(rows)
+    return [(cuts[k], cuts[k + 1]) for k in range(world)]
+
+
+def edge_flags(level_blocks, cols: int, band, R: int) -> np.ndarray:
+    """Per level: bit 0 if the band wrote blocks within R rows of its top edge,
+    bit 1 for the bottom edge (what fse_shard_levels reports)."""
+    lo, hi = band
+    out = np.zeros(len(level_blocks), dtype=np.int32)
+    for l, blocks in enumerate(level_blocks):
+        r = np.asarray(blocks, dtype=np.int64) // cols
+        r = r[(r >= lo) & (r < hi)]
+        if r.size:
+            out[l] = int((r < lo + R).any()) | (int((r >= hi - R).any()) << 1)
+    return out
+
+
+def exchange_plan(rank: int, world: int, bands, flags_all, level: int, R: int, B: int, H: int):
+    """(sends, recvs) of one level: lists of (peer, y0, y1) image-row ranges."""
+    lo, hi = bands[rank]
+    sends, recvs = [], []
+    if rank > 0:
+        if flags_all[rank][level] & 1:
+            sends.append((rank - 1, lo * B, min(H, (lo + R) * B)))
+        if flags_all[rank - 1][level] & 2:
+            recvs.append((rank - 1, max(0, (lo - R) * B), lo * B))
+    if rank < world - 1:
+        if flags_all[rank][level] & 2:
+            sends.append((rank + 1, max(0, (hi - R) * B), min(H, hi * B)))
+        if flags_all[rank + 1][level] & 1:
+            recvs.append((rank + 1, hi * B, min(H, (hi + R) * B)))
+    return sends, recvs
+
+
+def run_levels(executor, image, rank: int, world: int, bands, flags_all, n_levels: int, R: int,
+               B: int, H: int, dist, group=None) -> int:
+    """The protocol: run each level of the own band, then swap the halos the
+    level changed.  `image` is the rank's full-frame tensor (device or host);
+    row slices are contiguous views, sent and received in place.  Returns the
+    number of halo messages this rank sent."""
+    sent = 0
+    for l in range(n_levels):
+        executor.run(l)
+        if world == 1:
+            continue
+        sends, recvs = exchange_plan(rank, world, bands, flags_all, l, R, B, H)
+        if not sends and not recvs:
+            continue
+        ops = [dist.P2POp(dist.isend, image[y0:y1], peer, group) for peer, y0, y1 in sends]
+        ops += [dist.P2POp(dist.irecv, image[y0:y1], peer, group) for peer, y0, y1 in recvs]
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+        sent += len(sends)
+    return sent
+
+
+class ShardExecutor:
+    """GPU executor: one fse_shard_* session over a band of the rank's frame."""
+
+    def __init__(self, plan, band, image_dev, mask_dev, mask_out_dev, params: FseParams,
+                 precision: str, stream=None):
+        import torch
+
+        self.stream = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        dim = max(plan.max_wr, plan.max_wc, 1)
+        self._decay = DeviceContext.decay(params, dim)
+        code = _lib.FSE_F64 if precision == "fp64" else _lib.FSE_F32
+        pc = params.to_c()
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().fse_shard_open(
+            plan.handle, band[0], band[1], image_dev.data_ptr(), mask_dev.data_ptr(),
+            mask_out_dev.data_ptr() if mask_out_dev is not None else None, ctypes.byref(pc), code,
+            self._decay.data_ptr(), dim, self.stream, ctypes.byref(h)))
+        self.handle = h
+        n = ctypes.c_int32()
+        _lib.check(_lib.lib().fse_shard_levels(self.handle, ctypes.byref(n), None))
+        self.n_levels = n.value
+        fl = np.zeros(max(self.n_levels, 1), dtype=np.int32)
+        _lib.check(_lib.lib().fse_shard_levels(self.handle, ctypes.byref(n), _lib.ptr32(fl)))
+        self.flags = fl[: self.n_levels]
+
+    def run(self, level: int) -> None:
+        _lib.check(_lib.lib().fse_shard_run(self.handle, level, level + 1, self.stream))
+
+    def close(self) -> None:
+        if self.handle is not None and self.handle.value:
+            _lib.check(_lib.lib().fse_shard_close(self.handle, self.stream))
+            self.handle = None
+
+
+def conceal_strips(image, mask, params: FseParams, precision: str = "fp32", order: str = "optimized",
+                   group=None, gather: bool = True):
+    """Conceal one frame on all ranks of the default process group (one GPU per
+    rank).  Returns (image, mask) numpy arrays on rank 0 when gather=True (other
+    ranks get None), else this rank's band rows and its band."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    mask = np.ascontiguousarray(mask, dtype=np.uint8)
+    H, W = mask.shape
+    plan = build_plan(mask, params, order)
+    B = params.block_size
+    R = halo_rows(params)
+    processed = (plan.ranks() != np.iinfo(np.int32).max).reshape(plan.rows, plan.cols)
+    bands = band_partition(processed.sum(axis=1), world, R)
+    tdt = torch.float32 if precision == "fp32" else torch.float64
+    img_d = torch.as_tensor(np.ascontiguousarray(image)).to(device="cuda", dtype=tdt)
+    msk_d = torch.from_numpy(mask).cuda()
+    out_d = torch.empty_like(msk_d)
+    ex = ShardExecutor(plan, bands[rank], img_d, msk_d, out_d, params, precision)
+    flags_all = [ex.flags]
+    if world > 1:
+        t = torch.as_tensor(ex.flags, dtype=torch.int32, device="cuda")
+        gathered = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(gathered, t, group=group)
+        flags_all = [g.cpu().numpy() for g in gathered]
+    run_levels(ex, img_d, rank, world, bands, flags_all, ex.n_levels, R, B, H, dist, group)
+    ex.close()
+    lo, hi = bands[rank]
+    y0, y1 = lo * B, min(H, hi * B)
+    if not gather:
+        return img_d[y0:y1].double().cpu().numpy(), out_d[y0:y1].cpu().numpy(), bands[rank]
+    if world > 1:
+        if rank == 0:
+            for r in range(1, world):
+                a, b = bands[r][0] * B, min(H, bands[r][1] * B)
+                dist.recv(img_d[a:b], r, group)
+                dist.recv(out_d[a:b], r, group)
+        else:
+            dist.send(img_d[y0:y1].contiguous(), 0, group)
+            dist.send(out_d[y0:y1].contiguous(), 0, group)
+    if rank != 0:
+        return None
+    return img_d.double().cpu().numpy(), out_d.cpu().numpy()

@@ -30,6 +30,45 @@ def csr(ptr, blocks):
     return [blocks[ptr[k]:ptr[k + 1]].tolist() for k in range(len(ptr) - 1)]
 
 
+def block_owner(H, W, B):
+    rows, cols = -(-H // B), -(-W // B)
+    by = np.minimum(np.arange(H) // B, rows - 1)
+    bx = np.minimum(np.arange(W) // B, cols - 1)
+    return by[:, None] * cols + bx[None, :]
+
+
+def emulate_block(img, mask, b, ranks, owner, B, p, kernel="c"):
+    """Fit block b as the device does (classes from the ORIGINAL mask + ranks)
+    with the oracle kernel and write its LOST samples into img (any array with
+    numpy-style slicing, e.g. a torch CPU tensor)."""
+    H, W = mask.shape
+    cols = -(-W // B)
+    d = p.d
+    r, c = divmod(b, cols)
+    r0, r1, c0, c1 = r * B, min(r * B + B, H), c * B, min(c * B + B, W)
+    wr0, wr1, wc0, wc1 = max(0, r0 - d), min(H, r1 + d), max(0, c0 - d), min(W, c1 + d)
+    sub = mask[wr0:wr1, wc0:wc1]
+    own = owner[wr0:wr1, wc0:wc1]
+    lost = sub == O.LOST
+    cls = np.where(sub == O.RECONSTRUCTED, O.AREA_R, O.AREA_A).astype(np.uint8)
+    earlier = ranks[own] < ranks[b]
+    cls[lost & (own != b) & earlier] = O.AREA_R
+    cls[lost & (own != b) & ~earlier] = O.AREA_BO
+    cls[lost & (own == b)] = O.AREA_BI
+    vals = np.array(img[wr0:wr1, wc0:wc1], dtype=np.float64)
+    blk = O.extrapolate(vals, cls, (r0 - wr0, r1 - wr0, c0 - wc0, c1 - wc0), p, kernel)
+    assert blk is not None, f"plan scheduled a degenerate block {b}"
+    lostb = mask[r0:r1, c0:c1] == O.LOST
+    cur = np.array(img[r0:r1, c0:c1], dtype=np.float64)
+    cur[lostb] = blk[lostb]
+    if isinstance(img, np.ndarray):
+        img[r0:r1, c0:c1] = cur
+    else:  # torch CPU tensor (strip-protocol tests)
+        import torch
+
+        img[r0:r1, c0:c1] = torch.from_numpy(cur).to(img.dtype)
+
+
 def emulate_levels(image, mask, B, d, rho, delta, gamma, iterations, fft, ranks, levels, kernel="c",
                    shuffle_seed=0):
     """What the device does, on the CPU: for each level, every block classifies
@@ -39,30 +78,12 @@ def emulate_levels(image, mask, B, d, rho, delta, gamma, iterations, fft, ranks,
     rng = np.random.default_rng(shuffle_seed)
     img = np.array(image, dtype=np.float64, copy=True)
     H, W = img.shape
-    rows, cols = -(-H // B), -(-W // B)
-    by = np.minimum(np.arange(H) // B, rows - 1)
-    bx = np.minimum(np.arange(W) // B, cols - 1)
-    owner = by[:, None] * cols + bx[None, :]
+    owner = block_owner(H, W, B)
     p = O.Params(d=d, rho=rho, delta=delta, gamma=gamma, iterations=iterations, block_size=B,
                  fft_size=fft)
     for level in levels:
         for b in rng.permutation(level).tolist():
-            r, c = divmod(b, cols)
-            r0, r1, c0, c1 = r * B, min(r * B + B, H), c * B, min(c * B + B, W)
-            wr0, wr1, wc0, wc1 = max(0, r0 - d), min(H, r1 + d), max(0, c0 - d), min(W, c1 + d)
-            sub = mask[wr0:wr1, wc0:wc1]
-            own = owner[wr0:wr1, wc0:wc1]
-            lost = sub == O.LOST
-            cls = np.where(sub == O.RECONSTRUCTED, O.AREA_R, O.AREA_A).astype(np.uint8)
-            earlier = ranks[own] < ranks[b]
-            cls[lost & (own != b) & earlier] = O.AREA_R
-            cls[lost & (own != b) & ~earlier] = O.AREA_BO
-            cls[lost & (own == b)] = O.AREA_BI
-            vals = img[wr0:wr1, wc0:wc1].copy()
-            blk = O.extrapolate(vals, cls, (r0 - wr0, r1 - wr0, c0 - wc0, c1 - wc0), p, kernel)
-            assert blk is not None, f"plan scheduled a degenerate block {b}"
-            lost = mask[r0:r1, c0:c1] == O.LOST
-            img[r0:r1, c0:c1][lost] = blk[lost]
+            emulate_block(img, mask, b, ranks, owner, B, p, kernel)
     out_mask = mask.copy()
     done = ranks[owner] != np.iinfo(np.int32).max
     out_mask[(mask == O.LOST) & done] = O.RECONSTRUCTED

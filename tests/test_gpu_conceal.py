@@ -285,3 +285,63 @@ def test_config5_block_sizes_fp32_fast_path(B, F):
     truth = img.astype(np.float64)
     assert abs(psnr(truth, o32, mask) - psnr(truth, o64, mask)) <= FP32_PSNR_DB
     assert np.isfinite(o32).all()
+
+
+@pytest.mark.parametrize("prec,world", [("fp64", 2), ("fp32", 3)])
+def test_strip_shards_on_one_gpu_equal_whole_frame(prec, world):
+    """The C-ABI shard sessions (fse_shard_*) of a row-band partition, stepped
+    level by level with the halo copies of paper_2207_00233_b200.strips (done
+    here as device copies between the bands' images), reproduce the
+    whole-frame result bit for bit.  The NCCL transport itself is covered on
+    CPU by tests/test_strips.py."""
+    import torch
+
+    from paper_2207_00233_b200 import strips
+
+    img, mask = synth.config_scene(5)
+    img, mask = img[:256, :384].copy(), mask[:256, :384].copy()
+    H = img.shape[0]
+    p = P.FseParams(d=14, iterations=30, block_size=4, fft_size=64)
+    want, want_m, _ = P.conceal(img, mask, p, precision=prec)
+    plan = P.build_plan(mask, p)
+    R = strips.halo_rows(p)
+    processed = (plan.ranks() != np.iinfo(np.int32).max).reshape(plan.rows, plan.cols)
+    bands = strips.band_partition(processed.sum(axis=1), world, R)
+    tdt = torch.float32 if prec == "fp32" else torch.float64
+    imgs = [torch.from_numpy(img).cuda().to(tdt) for _ in range(world)]
+    msk = torch.from_numpy(mask).cuda()
+    outs = [torch.zeros_like(msk) for _ in range(world)]
+    exs = [strips.ShardExecutor(plan, bands[r], imgs[r], msk, outs[r], p, prec) for r in range(world)]
+    levels = plan.levels()
+    for r in range(world):
+        np.testing.assert_array_equal(exs[r].flags, strips.edge_flags(levels, plan.cols, bands[r], R))
+    flags_all = [e.flags for e in exs]
+    for l in range(plan.n_levels):
+        for e in exs:
+            e.run(l)
+        for r in range(world):
+            sends, _ = strips.exchange_plan(r, world, bands, flags_all, l, R, p.block_size, H)
+            for peer, y0, y1 in sends:
+                imgs[peer][y0:y1].copy_(imgs[r][y0:y1])
+    for e in exs:
+        e.close()
+    got = np.zeros_like(want)
+    got_m = np.zeros_like(want_m)
+    for r, (lo, hi) in enumerate(bands):
+        y0, y1 = lo * p.block_size, min(H, hi * p.block_size)
+        got[y0:y1] = imgs[r][y0:y1].double().cpu().numpy()
+        got_m[y0:y1] = outs[r][y0:y1].cpu().numpy()
+    assert got.tobytes() == want.tobytes()
+    np.testing.assert_array_equal(got_m, want_m)
+
+
+def test_conceal_strips_single_rank_equals_conceal():
+    from paper_2207_00233_b200 import strips
+
+    img, mask = synth.config_scene(5)
+    img, mask = img[:128, :256].copy(), mask[:128, :256].copy()
+    p = P.FseParams(d=14, iterations=30, block_size=4, fft_size=64)
+    want, want_m, _ = P.conceal(img, mask, p, precision="fp64")
+    got, got_m = strips.conceal_strips(img, mask, p, precision="fp64")
+    assert got.tobytes() == want.tobytes()
+    np.testing.assert_array_equal(got_m, want_m)
