@@ -54,7 +54,9 @@ def args_():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=4, choices=[3, 4])
+    ap.add_argument("--config", type=int, default=4, choices=[3, 4, 5])
+    ap.add_argument("--block", type=int, default=4, choices=[2, 4, 8],
+                    help="config 5 block size (FFT 32 / 64 / 128)")
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--frames", type=int, default=64)
     ap.add_argument("--guard", default=None,
@@ -446,6 +448,104 @@ def run_b200(a, rank, world, local_rank):
         dist.barrier()
 
 
+def run_strips_bench(a, rank, world, local_rank):
+    """BASELINE config 5: one 3840x2160 frame, 50% burst losses, B in {2,4,8}
+    (FFT 32/64/128), 100 iterations, fp32, spatially strip-sharded over the
+    ranks (paper_2207_00233_b200.strips).  A step = host plan (every rank, same
+    global plan) + shard levels with halo exchanges + result gather to rank 0."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2207_00233_b200 as P
+    from paper_2207_00233_b200 import _lib, strips, synth
+
+    torch.cuda.set_device(local_rank)
+    Bk = a.block
+    Fk = {2: 32, 4: 64, 8: 128}[Bk]
+    params = P.FseParams(d=D, rho=RHO, delta=DELTA, gamma=GAMMA, iterations=100, block_size=Bk,
+                         fft_size=Fk)
+    img, mask = synth.config_scene(5)
+    H, W = mask.shape
+    src = torch.from_numpy(img).cuda().float()
+    msk = torch.from_numpy(mask).cuda()
+    work = torch.empty_like(src)
+    out = torch.empty_like(msk)
+    R = strips.halo_rows(params)
+    grp = dist.group.WORLD if world > 1 else None
+    stats = {}
+
+    def step():
+        work.copy_(src)
+        t0 = time.perf_counter()
+        plan = P.build_plan(mask, params)
+        processed = (plan.ranks() != np.iinfo(np.int32).max).reshape(plan.rows, plan.cols)
+        bands = strips.band_partition(processed.sum(axis=1), world, R)
+        stats["plan_ms"] = 1e3 * (time.perf_counter() - t0)
+        stats["blocks"] = plan.n_processed
+        ex = strips.ShardExecutor(plan, bands[rank], work, msk, out, params, "fp32")
+        flags_all = [ex.flags]
+        if world > 1:
+            t = torch.as_tensor(ex.flags, dtype=torch.int32, device="cuda")
+            g = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(g, t)
+            flags_all = [x.cpu().numpy() for x in g]
+        stats["halo_msgs"] = strips.run_levels(ex, work, rank, world, bands, flags_all, ex.n_levels, R,
+                                               Bk, H, dist, grp)
+        stats["levels"] = ex.n_levels
+        ex.close()
+        if world > 1:  # gather the bands to rank 0
+            lo, hi = bands[rank]
+            if rank == 0:
+                for r in range(1, world):
+                    y0, y1 = bands[r][0] * Bk, min(H, bands[r][1] * Bk)
+                    dist.recv(work[y0:y1], r)
+            else:
+                dist.send(work[lo * Bk:min(H, hi * Bk)].contiguous(), 0)
+        return plan
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    lib = _lib.lib()
+    lib.fse_launch_count(1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        e0.record()
+        for _ in range(a.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    launches = int(lib.fse_launch_count(1))
+    if rank == 0:
+        blocks = stats["blocks"]
+        flop = counted_flops_per_block(100, Fk, Fk) * blocks
+        line = {
+            "metric": "lost_blocks_per_s", "value": blocks * a.steps / (ms * 1e-3), "unit": "blocks/s",
+            "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms / a.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded BASELINE generators, paper_2207_00233_b200/synth.py)",
+            "config": {"workload": f"config5: 3840x2160 synthetic luma, 50% burst 16x16 losses, FSE "
+                                   f"{Bk}x{Bk} / d=14 / FFT {Fk}x{Fk} / 100 it, optimized order, fp32, "
+                                   f"strip-sharded", "block": Bk, "fft": Fk,
+                       "parallelism": f"row bands x{world}, per-level halo exchange"},
+            "lost_mpixel_per_s": float((mask == 1).sum()) * a.steps / (ms * 1e-3) / 1e6,
+            "blocks_per_step": blocks, "levels_per_step": stats["levels"],
+            "host_plan_ms_per_step": stats["plan_ms"], "halo_messages_rank0": stats["halo_msgs"],
+            "counted_tflop_per_s": flop * a.steps / (ms * 1e-3) / 1e12,
+            "gpu_launches": launches, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
 def main():
     a = args_()
     rank = int(os.environ.get("RANK", 0))
@@ -463,7 +563,10 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_b200(a, rank, world, local_rank)
+        if a.config == 5:
+            run_strips_bench(a, rank, world, local_rank)
+        else:
+            run_b200(a, rank, world, local_rank)
     finally:
         if world > 1:
             dist.destroy_process_group()
