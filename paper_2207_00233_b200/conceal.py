@@ -239,7 +239,8 @@ def conceal(image, mask, params: FseParams | None = None, order: str = OPTIMIZED
 
 
 def conceal_batch(images, masks, params: FseParams | None = None, order: str = OPTIMIZED,
-                  precision: str = "fp32", plan_threads: int = 0, reports: bool = True):
+                  precision: str = "fp32", plan_threads: int = 0, reports: bool = True,
+                  out_images=None, out_masks=None):
     """Frame-parallel concealment of equally sized frames: one plan per frame
     (C++ threads, overlapped with the upload), every dependency level of every
     frame in one launch.
@@ -247,7 +248,10 @@ def conceal_batch(images, masks, params: FseParams | None = None, order: str = O
     images: [n, H, W] numpy array or CPU torch tensor (any real dtype; pinned
     torch tensors upload asynchronously), masks: [n, H, W] uint8 likewise.
     Returns (images [n, H, W] numpy in the compute dtype — float64 for "fp64",
-    float32 for "fp32" —, masks [n, H, W] uint8, reports or None)."""
+    float32 for "fp32" —, masks [n, H, W] uint8, reports or None).
+    out_images / out_masks: optional preallocated (pinned) CPU tensors of the
+    output shapes and dtypes; results land there (streaming callers reuse them
+    instead of pinning fresh buffers every call)."""
     if params is None:
         params = FseParams()
     if order not in ORDERS:
@@ -274,8 +278,13 @@ def conceal_batch(images, masks, params: FseParams | None = None, order: str = O
     out_d = torch.empty_like(msk_d)
     plans = plan_and_run(list(msks.numpy()), list(img_d), list(msk_d), list(out_d), params,
                          precision, order, plan_threads)
-    out_img = torch.empty(img_d.shape, dtype=tdt, pin_memory=True)
-    out_msk = torch.empty(out_d.shape, dtype=torch.uint8, pin_memory=True)
+    out_img = out_images if out_images is not None else torch.empty(img_d.shape, dtype=tdt, pin_memory=True)
+    out_msk = out_masks if out_masks is not None else torch.empty(out_d.shape, dtype=torch.uint8,
+                                                                   pin_memory=True)
+    if tuple(out_img.shape) != tuple(img_d.shape) or out_img.dtype != tdt:
+        raise ValueError("out_images has the wrong shape or dtype")
+    if tuple(out_msk.shape) != tuple(out_d.shape) or out_msk.dtype != torch.uint8:
+        raise ValueError("out_masks has the wrong shape or dtype")
     out_img.copy_(img_d, non_blocking=True)
     out_msk.copy_(out_d, non_blocking=True)
     torch.cuda.current_stream().synchronize()

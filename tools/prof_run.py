@@ -22,8 +22,17 @@ L.fse_set_guard(t0, t1)
 sc = [synth.config_scene(a.config, f) for f in range(a.frames)]
 imgs = np.stack([s[0] for s in sc]); msks = np.stack([s[1] for s in sc])
 p = P.FseParams(d=14, iterations=a.iters, block_size=a.block, fft_size=a.fft)
-for _ in range(a.reps):
-    out, om, _ = P.conceal_batch(imgs, msks, p, precision=a.precision, reports=False)
+import torch
+tdt = torch.float32 if a.precision == "fp32" else torch.float64
+img_d = torch.from_numpy(imgs).cuda().to(tdt)
+msk_d = torch.from_numpy(msks).cuda()
+out_d = torch.empty_like(msk_d)
+plans = P.build_plans(list(msks), p)
+for _ in range(a.reps):  # one call, every level of all frames merged (no chunking)
+    work = img_d.clone()
+    P.run_frames_device(plans, list(work), list(msk_d), list(out_d), p, a.precision)
+torch.cuda.synchronize()
+out = work.cpu().numpy()
 if a.stats:
     o64, _, _ = P.conceal_batch(imgs, msks, p, precision="fp64", reports=False)
     lost = msks == 1
