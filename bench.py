@@ -104,7 +104,16 @@ class ClockSampler:
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
+        # nvidia-smi -i takes a physical index or a UUID; the UUID survives any
+        # CUDA_VISIBLE_DEVICES remapping
         self.index = index
+        try:
+            import torch
+
+            u = str(torch.cuda.get_device_properties(index % max(1, torch.cuda.device_count())).uuid)
+            self.index = u if u.startswith("GPU-") else f"GPU-{u}"
+        except Exception:
+            pass
         self.rows = []
         self._stop = threading.Event()
         self._t = None
@@ -115,8 +124,9 @@ class ClockSampler:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                       "--format=csv,noheader,nounits"], capture_output=True,
                                      text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                row = [x.strip() for x in out.split(",")] if out else []
+                if len(row) == 6:
+                    self.rows.append(row)
             except Exception:
                 pass
             self._stop.wait(0.2)
@@ -223,6 +233,14 @@ def run_reference(a, rank, world):
 
 # ------------------------------------------------------------------ B200 arm
 
+def _allreduce(torch, dist, values, op):
+    """all_reduce of a few floats on the backend's device (CPU for gloo)."""
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor(values, dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=op)
+    return t.cpu().tolist()
+
+
 def measure_peaks(torch, lib):
     """Arithmetic throughput of this GPU (roofline denominators), CUDA events:
     FFMA, FFMA2 (packed f32x2, what the fp32 kernel issues) and DFMA."""
@@ -255,7 +273,7 @@ def run_b200(a, rank, world, local_rank):
     import paper_2207_00233_b200 as P
     from paper_2207_00233_b200 import _lib
 
-    torch.cuda.set_device(local_rank)
+    torch.cuda.set_device(local_rank % max(1, torch.cuda.device_count()))
     lib = _lib.lib()
     if a.guard is not None:
         t0_, t1_ = (-1.0, 0.0) if a.guard == "off" else (float(x) for x in a.guard.split(","))
@@ -273,7 +291,10 @@ def run_b200(a, rank, world, local_rank):
     mout = torch.empty_like(msks_d)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     masks_np = list(msks_h.numpy())
-    plan_threads = 0
+    # share the host cores between the ranks of this node (the C++ planner
+    # otherwise starts hardware_concurrency threads in every rank)
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    plan_threads = max(1, (os.cpu_count() or 1) // max(1, local_world)) if world > 1 else 0
 
     # work accounting from one plan set
     plans = P.build_plans(masks_np, params, "optimized", plan_threads)
@@ -298,9 +319,7 @@ def run_b200(a, rank, world, local_rank):
         ms = e0.elapsed_time(e1)
         del keep
         if world > 1:
-            t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
+            ms = _allreduce(torch, dist, [ms], dist.ReduceOp.MAX)[0]
         return ms
 
     def measure(precision, sample_clocks):
@@ -346,10 +365,9 @@ def run_b200(a, rank, world, local_rank):
     other_prec = "fp64" if a.precision == "fp32" else "fp32"
     other = None if a.no_second else measure(other_prec, False)
 
-    tot = torch.tensor([blocks_rank, lost_px_rank], dtype=torch.float64, device="cuda")
+    blocks_all, lost_px_all = float(blocks_rank), float(lost_px_rank)
     if world > 1:
-        dist.all_reduce(tot)
-    blocks_all, lost_px_all = float(tot[0]), float(tot[1])
+        blocks_all, lost_px_all = _allreduce(torch, dist, [blocks_rank, lost_px_rank], dist.ReduceOp.SUM)
     value = blocks_all * a.steps / (head["ms"] * 1e-3)
 
     # roofline of the dominant kernel (the level launches): counted FLOPs per
@@ -465,7 +483,7 @@ def run_strips_bench(a, rank, world, local_rank):
     import paper_2207_00233_b200 as P
     from paper_2207_00233_b200 import _lib, strips, synth
 
-    torch.cuda.set_device(local_rank)
+    torch.cuda.set_device(local_rank % max(1, torch.cuda.device_count()))
     Bk = a.block
     Fk = {2: 32, 4: 64, 8: 128}[Bk]
     params = P.FseParams(d=D, rho=RHO, delta=DELTA, gamma=GAMMA, iterations=100, block_size=Bk,
@@ -491,7 +509,8 @@ def run_strips_bench(a, rank, world, local_rank):
         ex = strips.ShardExecutor(plan, bands[rank], work, msk, out, params, "fp32")
         flags_all = [ex.flags]
         if world > 1:
-            t = torch.as_tensor(ex.flags, dtype=torch.int32, device="cuda")
+            dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+            t = torch.as_tensor(ex.flags, dtype=torch.int32, device=dev)
             g = [torch.empty_like(t) for _ in range(world)]
             dist.all_gather(g, t)
             flags_all = [x.cpu().numpy() for x in g]
@@ -527,9 +546,7 @@ def run_strips_bench(a, rank, world, local_rank):
         dist.barrier()
     ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = _allreduce(torch, dist, [ms], dist.ReduceOp.MAX)[0]
     launches = int(lib.fse_launch_count(1))
     if rank == 0:
         blocks = stats["blocks"]
@@ -566,8 +583,16 @@ def main():
     import torch.distributed as dist
 
     if world > 1:
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        # FSE_BENCH_BACKEND=gloo: functional multi-rank check on a single GPU
+        # (ranks share the device; only host-side barriers/reductions, no
+        # kernel waits on another rank) — numbers from such a run are not valid
+        backend = os.environ.get("FSE_BENCH_BACKEND", "nccl")
+        dev = local_rank % max(1, torch.cuda.device_count())
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     try:
         if a.config == 5:
             run_strips_bench(a, rank, world, local_rank)
