@@ -181,6 +181,15 @@ int fse_shard_run(FseShard *shard, int32_t level_lo, int32_t level_hi, void *str
 /* mask pass over the band's rows (if mask_out was given) and release */
 int fse_shard_close(FseShard *shard, void *stream);
 
+/* Output epilogue over n frames of npix samples each (device pointers, frames
+ * contiguous): out_u8 (or NULL) = floor(clip(x, 0, 255) + 0.5), the rounding
+ * of fsefill.image.save_pgm (image.py:79-88); if sums != NULL, per frame f
+ * sums[2f] = sum (truth - x)^2 and sums[2f+1] = count over samples whose mask
+ * is not KNOWN — the terms of fsefill.evalkit.psnr (evalkit.py:67-81).
+ * truth: uint8 originals; masks: uint8 (pre- or post-concealment). */
+int fse_quantize_psnr(int32_t n, int64_t npix, const void *images, int32_t dtype, const uint8_t *truth,
+                      const uint8_t *masks, uint8_t *out_u8, double *sums, void *stream);
+
 /* Count of kernel launches issued since the last reset (bench.py gpu_launches). */
 int64_t fse_launch_count(int32_t reset);
 

@@ -23,6 +23,7 @@ EXPORTS = (
     "fse_launch_count", "fse_timing_enable", "fse_timing_read", "fse_fma_probe",
     "fse_set_guard", "fse_guard_redo_count", "fse_set_dataflow",
     "fse_shard_open", "fse_shard_levels", "fse_shard_run", "fse_shard_close",
+    "fse_quantize_psnr",
 )
 
 
@@ -91,6 +92,7 @@ def lib():
         L.fse_shard_levels.argtypes = [_vp, _pi32, _pi32]
         L.fse_shard_run.argtypes = [_vp, _i32, _i32, _vp]
         L.fse_shard_close.argtypes = [_vp, _vp]
+        L.fse_quantize_psnr.argtypes = [_i32, ctypes.c_int64, _vp, _i32, _vp, _vp, _vp, _vp, _vp]
         L.fse_guard_redo_count.restype = ctypes.c_int64
         L.fse_launch_count.argtypes = [_i32]
         L.fse_launch_count.restype = ctypes.c_int64

@@ -291,3 +291,41 @@ def conceal_batch(images, masks, params: FseParams | None = None, order: str = O
     wall = time.perf_counter() - t0
     reps = [_report(p, order, 1, wall) for p in plans] if reports else None
     return out_img.numpy(), out_msk.numpy(), reps
+
+
+def quantize_psnr_device(images_dev, truth_dev=None, masks_dev=None, quantize: bool = True):
+    """Output epilogue on device frames [n, H, W] (fp32/fp64): uint8 frames with
+    save_pgm rounding (image.py:79-88) and, given the uint8 originals and the
+    masks, the per-frame PSNR over non-KNOWN samples (evalkit.psnr,
+    evalkit.py:67-81; +inf when equal, ValueError on an empty region).
+    Returns (u8 tensor or None, list of PSNR dB or None)."""
+    import torch
+
+    x = images_dev
+    if x.dim() == 2:
+        x = x[None]
+    n = x.shape[0]
+    npix = x.shape[1] * x.shape[2]
+    code = _lib.FSE_F64 if x.dtype == torch.float64 else _lib.FSE_F32
+    out = torch.empty(x.shape, dtype=torch.uint8, device=x.device) if quantize else None
+    sums = None
+    if truth_dev is not None:
+        if masks_dev is None:
+            raise ValueError("psnr needs the masks")
+        sums = torch.empty((n, 2), dtype=torch.float64, device=x.device)
+    s = torch.cuda.current_stream().cuda_stream
+    t = truth_dev.reshape(x.shape) if truth_dev is not None else None
+    m = masks_dev.reshape(x.shape) if masks_dev is not None else None
+    _lib.check(_lib.lib().fse_quantize_psnr(
+        n, npix, x.contiguous().data_ptr(), code, t.data_ptr() if t is not None else None,
+        m.data_ptr() if m is not None else None, out.data_ptr() if out is not None else None,
+        sums.data_ptr() if sums is not None else None, s))
+    psnrs = None
+    if sums is not None:
+        psnrs = []
+        for se, cnt in sums.cpu().tolist():
+            if cnt == 0:
+                raise ValueError("mask selects no samples to compare")
+            mse = se / cnt
+            psnrs.append(float("inf") if mse == 0.0 else 10.0 * np.log10(255.0 ** 2 / mse))
+    return out, psnrs

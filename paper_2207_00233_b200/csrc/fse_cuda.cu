@@ -84,6 +84,39 @@ __global__ void dfma_probe_kernel(float *out, int iters, double a, double b) {
     if (s == 12345.678) out[0] = (float)s;
 }
 
+// Output epilogue, one HBM pass per frame: save_pgm quantisation
+// floor(clip(x, 0, 255) + 0.5) (image.py:79-88) into uint8, and the squared
+// error against the original over the samples the mask marks non-KNOWN
+// (evalkit.psnr, evalkit.py:67-81).  Per-frame sums land in sums[2f] (squared
+// error, fp64) and sums[2f+1] (count); frame f = blockIdx.y.
+template <typename T>
+__global__ void quantize_psnr_kernel(const T *img, long long frame_stride, long long npix,
+                                     const uint8_t *truth, const uint8_t *mask, uint8_t *out_u8,
+                                     double *sums) {
+    const int f = blockIdx.y;
+    const T *im = img + (size_t)f * frame_stride;
+    double se = 0.0, cnt = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < npix;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double v = (double)im[i];
+        if (out_u8) out_u8[(size_t)f * npix + i] = (uint8_t)floor(fmin(fmax(v, 0.0), 255.0) + 0.5);
+        if (sums && mask[(size_t)f * npix + i] != FSE_KNOWN) {
+            const double d = (double)truth[(size_t)f * npix + i] - v;
+            se += d * d;
+            cnt += 1.0;
+        }
+    }
+    if (!sums) return;
+    for (int off = 16; off; off >>= 1) {
+        se += __shfl_xor_sync(0xffffffffu, se, off);
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(sums + 2 * f, se);
+        atomicAdd(sums + 2 * f + 1, cnt);
+    }
+}
+
 // LOST samples of concealed blocks become RECONSTRUCTED (conceal.py:65-66)
 __global__ void finalize_masks_kernel(const FrameDesc *frames, int n, int H, int W, int B, int cols,
                                       int y0, int y1) {
@@ -168,6 +201,31 @@ int fse_timing_read(double *ms, int64_t *window_launches, int64_t *calls) {
     if (window_launches) *window_launches = fse::g_timing.window_launches;
     if (calls) *calls = n;
     fse::g_timing.window_launches = 0;
+    return FSE_OK;
+}
+
+int fse_quantize_psnr(int32_t n, int64_t npix, const void *images, int32_t dtype, const uint8_t *truth,
+                      const uint8_t *masks, uint8_t *out_u8, double *sums, void *stream) {
+    if (n < 0 || npix < 0 || !images || (sums && (!truth || !masks)) || (!sums && !out_u8))
+        return fail(FSE_EINVAL, "bad quantize/psnr arguments");
+    if (dtype != FSE_F64 && dtype != FSE_F32) return fail(FSE_EINVAL, "dtype");
+    if (n == 0 || npix == 0) return FSE_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (sums) {
+        cudaError_t ce = cudaMemsetAsync(sums, 0, sizeof(double) * 2 * n, s);
+        if (ce != cudaSuccess) return fail(FSE_ECUDA, cudaGetErrorString(ce));
+    }
+    const int gx = (int)std::max<long long>(1, std::min<long long>((npix + 255) / 256, 148LL * 4));
+    const dim3 grid(gx, n);
+    if (dtype == FSE_F32)
+        fse::quantize_psnr_kernel<float><<<grid, 256, 0, s>>>((const float *)images, npix, npix, truth, masks,
+                                                             out_u8, sums);
+    else
+        fse::quantize_psnr_kernel<double><<<grid, 256, 0, s>>>((const double *)images, npix, npix, truth,
+                                                              masks, out_u8, sums);
+    cudaError_t ce = cudaGetLastError();
+    if (ce != cudaSuccess) return fail(FSE_ECUDA, cudaGetErrorString(ce));
+    fse::g_launches.fetch_add(1, std::memory_order_relaxed);
     return FSE_OK;
 }
 

@@ -389,3 +389,25 @@ def test_full_size_fp64_blocks_match_oracle_on_their_snapshots(config, B, F, ite
         assert O.canonical_picks(picks[b], (F, F)) == O.canonical_picks(opk, (F, F)), b
         lb = mask[r0:r1, c0:c1] == O.LOST
         assert np.max(np.abs(out[r0:r1, c0:c1][lb] - blk[lb])) <= 1e-6, b
+
+
+def test_quantize_psnr_epilogue_matches_reference_semantics():
+    """fse_quantize_psnr: save_pgm rounding (image.py:79-88) and evalkit.psnr
+    (evalkit.py:67-81) over non-KNOWN samples, on device, for fp32 and fp64."""
+    import torch
+
+    rng = np.random.default_rng(3)
+    n, H, W = 3, 40, 56
+    truth = rng.integers(0, 256, (n, H, W)).astype(np.uint8)
+    mask = (rng.uniform(size=(n, H, W)) < 0.3).astype(np.uint8)
+    mask[1][mask[1] == 1] = 2  # post-concealment mask states count too
+    vals = truth + rng.normal(0, 9, (n, H, W))
+    vals[0, 0, :6] = [-3.0, 0.5, 1.5, 254.5, 255.49, 300.0]  # clamping and half-up ties
+    for dt in (torch.float32, torch.float64):
+        x = torch.from_numpy(vals).to(dt)
+        u8, ps = P.quantize_psnr_device(x.cuda(), torch.from_numpy(truth).cuda(), torch.from_numpy(mask).cuda())
+        xv = x.double().numpy()
+        np.testing.assert_array_equal(u8.cpu().numpy(), np.floor(np.clip(xv, 0, 255) + 0.5).astype(np.uint8))
+        for f in range(n):
+            want = psnr(truth[f].astype(np.float64), xv[f], mask[f])
+            assert abs(ps[f] - want) <= 1e-9 * abs(want)
