@@ -411,3 +411,32 @@ def test_quantize_psnr_epilogue_matches_reference_semantics():
         for f in range(n):
             want = psnr(truth[f].astype(np.float64), xv[f], mask[f])
             assert abs(ps[f] - want) <= 1e-9 * abs(want)
+
+
+@pytest.mark.parametrize("shape,B,F,prec", [((37, 53), 4, 64, "fp64"), ((10, 12), 4, 32, "fp64"),
+                                            ((37, 53), 4, 64, "fp32"), ((70, 45), 8, 128, "fp32"),
+                                            ((33, 31), 2, 32, "fp64")])
+def test_ragged_and_tiny_frames_fast_path_vs_oracle(shape, B, F, prec):
+    """Ragged block grids and frames smaller than a window through the fast
+    kernels, against the oracle pipeline (fp64: 1e-6; fp32: PSNR parity)."""
+    H, W = shape
+    rng = np.random.default_rng(H * W + B)
+    yy, xx = np.mgrid[0:H, 0:W]
+    img = np.clip(128 + 50 * np.sin(0.21 * xx + 0.13 * yy) + rng.normal(0, 2, shape), 0, 255).round()
+    mask = np.zeros(shape, np.uint8)
+    mask[rng.uniform(size=shape) < 0.0] = 1
+    for _ in range(4):
+        r0, c0 = int(rng.integers(0, H - 3)), int(rng.integers(0, W - 3))
+        mask[r0:r0 + int(rng.integers(2, 9)), c0:c0 + int(rng.integers(2, 9))] = 1
+    img[mask == 1] = 0
+    p = P.FseParams(d=14, iterations=25, block_size=B, fft_size=F)
+    out, om, rep = P.conceal(img, mask, p, precision=prec)
+    o_img, o_msk, o_rep = O.conceal(img, mask, O.Params(d=14, iterations=25, block_size=B, fft_size=(F, F)),
+                                    "optimized", kernel="auto")
+    assert rep.batches == o_rep.batches
+    np.testing.assert_array_equal(om, o_msk)
+    if prec == "fp64":
+        assert np.max(np.abs(out - o_img)) <= 1e-6
+    else:
+        truth = img.astype(np.float64)
+        assert abs(psnr(truth, out, mask) - psnr(truth, o_img, mask)) <= FP32_PSNR_DB
