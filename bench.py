@@ -54,7 +54,7 @@ def args_():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=4, choices=[3, 4, 5])
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--block", type=int, default=4, choices=[2, 4, 8],
                     help="config 5 block size (FFT 32 / 64 / 128)")
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
@@ -472,6 +472,79 @@ def run_b200(a, rank, world, local_rank):
         dist.barrier()
 
 
+def run_small_bench(a, rank, world, local_rank):
+    """BASELINE configs 1 and 2: one 512x512 frame, B=4 / d=14 / FFT 64 /
+    100 it.  Config 1: fp64, optimized order.  Config 2: optimized vs line-scan
+    order in fp32 and fp64 (the PSNR difference and the speed-up BASELINE asks
+    for).  Replicas only: every rank runs the same frame (these configs do not
+    shard).  A step = host plan + device levels + mask pass on resident inputs."""
+    import torch
+
+    import paper_2207_00233_b200 as P
+    from paper_2207_00233_b200 import _lib, synth
+
+    torch.cuda.set_device(local_rank % max(1, torch.cuda.device_count()))
+    params = P.FseParams(d=D, rho=RHO, delta=DELTA, gamma=GAMMA, iterations=100, block_size=B, fft_size=F)
+    img, mask = synth.config_scene(a.config)
+    truth = img.astype(np.float64)
+    msk = torch.from_numpy(mask).cuda()
+    out = torch.empty_like(msk)
+    lib = _lib.lib()
+
+    def run(order, precision):
+        tdt = torch.float32 if precision == "fp32" else torch.float64
+        src = torch.from_numpy(img).cuda().to(tdt)
+        work = torch.empty_like(src)
+
+        def step():
+            work.copy_(src)
+            plan = P.build_plan(mask, params, order)
+            P.run_frames_device([plan], [work], [msk], [out], params, precision)
+            return plan
+
+        for _ in range(a.warmup):
+            step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(a.steps):
+            plan = step()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / a.steps
+        res = work.double().cpu().numpy()
+        region = mask != 0
+        mse = float(np.mean((truth[region] - res[region]) ** 2))
+        return {"ms": ms, "blocks": plan.n_processed, "levels": plan.n_levels, "batches": plan.n_batches,
+                "psnr_db": 10 * np.log10(255.0 ** 2 / mse)}
+
+    lib.fse_launch_count(1)
+    combos = [("optimized", "fp64")] if a.config == 1 else [
+        ("optimized", "fp32"), ("linescan", "fp32"), ("optimized", "fp64"), ("linescan", "fp64")]
+    res = {f"{o}_{p}": run(o, p) for o, p in combos}
+    launches = int(lib.fse_launch_count(1))
+    head = res["optimized_fp64" if a.config == 1 else "optimized_fp32"]
+    if rank == 0:
+        line = {
+            "metric": "lost_blocks_per_s", "value": head["blocks"] / (head["ms"] * 1e-3), "unit": "blocks/s",
+            "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": head["ms"],
+            "higher_is_better": True, "scaling": "replicas", "vs_baseline": None,
+            "dtype": "f64" if a.config == 1 else "f32",
+            "data": "synthetic (seeded BASELINE generators, paper_2207_00233_b200/synth.py)",
+            "config": {"workload": f"config{a.config}: 512x512 synthetic, "
+                                   + ("10% isolated" if a.config == 1 else "20% horizontal bursts")
+                                   + " 16x16 losses, FSE 4x4 / d=14 / FFT 64x64 / 100 it"},
+            "lost_mpixel_per_s": float((mask == 1).sum()) / (head["ms"] * 1e-3) / 1e6,
+            "runs": res, "gpu_launches": launches,
+        }
+        if a.config == 2:
+            for p in ("fp32", "fp64"):
+                o, l = res[f"optimized_{p}"], res[f"linescan_{p}"]
+                line[f"{p}_optimized_minus_linescan_psnr_db"] = o["psnr_db"] - l["psnr_db"]
+                line[f"{p}_optimized_speedup_over_linescan"] = l["ms"] / o["ms"]
+        print(json.dumps(line), flush=True)
+
+
 def run_strips_bench(a, rank, world, local_rank):
     """BASELINE config 5: one 3840x2160 frame, 50% burst losses, B in {2,4,8}
     (FFT 32/64/128), 100 iterations, fp32, spatially strip-sharded over the
@@ -596,6 +669,8 @@ def main():
     try:
         if a.config == 5:
             run_strips_bench(a, rank, world, local_rank)
+        elif a.config in (1, 2):
+            run_small_bench(a, rank, world, local_rank)
         else:
             run_b200(a, rank, world, local_rank)
     finally:
