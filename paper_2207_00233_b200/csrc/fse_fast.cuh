@@ -585,12 +585,16 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
             pim = gwin.y / tot;
         }
         const bool selfc = ((2 * a) & (F - 1)) == 0 && ((2 * b) & (F - 1)) == 0;
-        if (t == 0 && picks_out) {
-            picks_out[2 * it] = a;
-            picks_out[2 * it + 1] = b;
-            if constexpr (MODE == 1) {
-                plog[2 * it] = pre;
-                plog[2 * it + 1] = pim;
+        // single-thread bookkeeping behind a warp-uniform branch, so the other
+        // warps do not issue its predicated stores
+        if (warp == 0 && picks_out) {
+            if (lane == 0) {
+                picks_out[2 * it] = a;
+                picks_out[2 * it + 1] = b;
+                if constexpr (MODE == 1) {
+                    plog[2 * it] = pre;
+                    plog[2 * it + 1] = pim;
+                }
             }
         }
         // self-conjugate: gamma * Re(p) * W[k - j] == (gamma Re(p) / 2) (W[k-j] + W[k+j])
@@ -602,7 +606,9 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
 
         // ---- (2) log the pick for the block model (synthesised after the loop)
         if constexpr (MODE == 0) {
-            if (t == 0) hist[it] = PickRec<T>{a, b, gpr, gpi};
+            if (warp == 0) {
+                if (lane == 0) hist[it] = PickRec<T>{a, b, gpr, gpi};
+            }
         }
         if (it + 1 == I) break;  // the last spectrum update is never observed
 
