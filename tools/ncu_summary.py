@@ -30,7 +30,11 @@ KEYS = ["Duration", "Elapsed Cycles", "SM Frequency", "Registers Per Thread", "D
         "Block Limit Registers", "Block Limit Shared Mem", "Theoretical Occupancy", "Achieved Occupancy",
         "Compute (SM) Throughput", "Executed Ipc Active", "Issue Slots Busy", "Memory Throughput",
         "DRAM Throughput", "L1/TEX Hit Rate", "L2 Hit Rate", "Grid Size", "Block Size"]
-RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__inst_executed.sum",
+RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "dram__bytes.sum.per_second",
+       "dram__bytes_read.sum.pct_of_peak_sustained_elapsed",
+       "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+       "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+       "derived__memory_l1_wavefronts_shared_excessive", "smsp__inst_executed.sum",
        "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
        "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
