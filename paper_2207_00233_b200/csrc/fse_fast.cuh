@@ -35,8 +35,12 @@
 
 namespace fse {
 
-template <typename T_, int F_, int NW_>
+template <typename T_, int F_, int NW_, bool EXT_ = true>
 struct FastCfg {
+    // EXT: row-extended W (rows -F/2..F, no modulo on the gathers).  !EXT: the
+    // plain F-row plane with a per-bin wrap select (2/3 of the shared memory;
+    // used where the extended plane would cost occupancy, i.e. fp64 at F = 64).
+    static constexpr bool EXT = EXT_;
     using T = T_;
     using T2 = typename V2<T_>::type;
     static constexpr int F = F_;
@@ -74,7 +78,7 @@ struct FastLayout {
 
 template <typename T>
 __host__ __device__ inline FastLayout fast_layout(int F, int NW, int Mmax, int Nmax, int model_n,
-                                                  int iters) {
+                                                  int iters, bool ext = true) {
     FastLayout L;
     const size_t c2 = 2 * sizeof(T);
     size_t o = 0;
@@ -102,11 +106,23 @@ __host__ __device__ inline FastLayout fast_layout(int F, int NW, int Mmax, int N
     L.yw = yb;
     L.xs = 2 * yb;
     L.ws = L.xs + xb;
-    // partials live above the W half-plane rows [HS, HE), so the w-plane
-    // combine can store W rows directly
-    L.part = (2 * yb + 2 * xb > HE) ? 2 * yb + 2 * xb : HE;
-    size_t bigb = L.part + pb;
-    if (bigb < EXT) bigb = EXT;
+    size_t bigb;
+    if (ext) {
+        // partials live above the W half-plane rows [HS, HE), so the w-plane
+        // combine can store W rows directly
+        L.part = (2 * yb + 2 * xb > HE) ? 2 * yb + 2 * xb : HE;
+        bigb = L.part + pb;
+        if (bigb < EXT) bigb = EXT;
+    } else {
+        // plain plane: half rows 0..F/2 at [0, HEc); partials above both the
+        // Y planes (read by the partials) and the half rows (written by the
+        // w combine); xs / ws are dead once the partials start
+        const size_t HEc = (size_t)(F / 2 + 1) * F * c2, FULL = (size_t)F * F * c2;
+        L.part = 2 * yb > HEc ? 2 * yb : HEc;
+        bigb = L.part + pb;
+        if (bigb < L.ws + xb) bigb = L.ws + xb;
+        if (bigb < FULL) bigb = FULL;
+    }
     (void)HS;
     (void)HE;
     L.total = L.big + bigb;
@@ -430,17 +446,25 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
         const int u = u0 + RSTEP * j;
-        if (u < R1) Wext[(u + F / 2) * F + v] = combine(u);
+        if (u < R1) Wext[(u + (C::EXT ? F / 2 : 0)) * F + v] = combine(u);
     }
     __syncthreads();
+    if constexpr (!C::EXT) {
+        // plain plane: rows F/2+1 .. F-1 by W[r][c] = conj W[F-r][-c]
+        for (int idx = t; idx < (F / 2 - 1) * F; idx += NT) {
+            const int rr = F / 2 + 1 + idx / F, c = idx % F;
+            const T2 src = Wext[(F - rr) * F + ((F - c) & (F - 1))];
+            Wext[rr * F + c] = T2{src.x, -src.y};
+        }
+    }
     // extension rows: W[-s] = conj W[s] reflected, W[F] = W[0]
-    for (int idx = t; idx < (F / 2) * F; idx += NT) {
+    for (int idx = t; C::EXT && idx < (F / 2) * F; idx += NT) {
         const int rr = idx / F, c = idx - rr * F;  // ext row rr in [0, F/2): W row rr - F/2
         const int s = F / 2 - rr;                  // W row -s, s in [1, F/2]
         const T2 src = Wext[(s + F / 2) * F + ((F - c) & (F - 1))];
         Wext[rr * F + c] = T2{src.x, -src.y};
     }
-    for (int idx = t; idx < (F / 2) * F; idx += NT) {
+    for (int idx = t; C::EXT && idx < (F / 2) * F; idx += NT) {
         const int rr = F + 1 + idx / F, c = idx % F;  // ext row rr in (F, 3F/2]: W row rr - F/2
         const int s = rr - F / 2;                     // in (F/2, F]
         T2 val;
@@ -614,8 +638,13 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
 
         // ---- (3) spectrum update by the shifted weight spectrum + next argmax
         const int cm = (v - b) & (F - 1), cp = (v + b) & (F - 1);
-        const T2 *lo = Wext + (u0 - a + F / 2) * F + cm;
-        const T2 *hi = Wext + (u0 + a + F / 2) * F + cp;
+        // EXT: rows u-a and u+a are in the extended plane as they are.
+        // plain: row (u0 - a + RSTEP j) mod F wraps once over the j range (below
+        // 0), row (u0 + a + RSTEP j) wraps only at F; pick the base per j.
+        const int x0 = u0 - a, y0 = u0 + a;
+        const T2 *lo = Wext + (C::EXT ? (x0 + F / 2) * F : x0 * F) + cm;
+        const T2 *hi = Wext + (C::EXT ? (y0 + F / 2) * F : y0 * F) + cp;
+        const T2 *loW = lo + F * F, *hiW = hi - F * F;  // plain plane: wrapped bases
         k1 = 0;
         k2 = 0;
         best = (T)-1;
@@ -631,8 +660,13 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
                 const int j = j0 + q;
                 const bool inr = j < NB && ((j < NB - 1) || (C::NSEGS % NW == 0) || (u0 + RSTEP * j < R1));
                 if (inr) {
-                    wl[q] = lo[j * RSTEP * F];
-                    wh[q] = hi[j * RSTEP * F];
+                    if constexpr (C::EXT) {
+                        wl[q] = lo[j * RSTEP * F];
+                        wh[q] = hi[j * RSTEP * F];
+                    } else {
+                        wl[q] = (x0 + RSTEP * j < 0 ? loW : lo)[j * RSTEP * F];
+                        wh[q] = (y0 + RSTEP * j >= F ? hiW : hi)[j * RSTEP * F];
+                    }
                 }
             }
 #pragma unroll

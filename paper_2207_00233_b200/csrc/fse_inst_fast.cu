@@ -10,7 +10,7 @@ namespace fse {
 // F = 64: 66 row segments of the half plane over 6 warps -> 11 bins per thread
 // (4 warps / 17 bins measured 5% slower: fewer warps to hide latency).
 // F = 32: 17 row segments over 6 warps -> 3 bins per thread.
-template <typename T> using Fast64 = FastCfg<T, 64, 6>;
+template <typename T> using Fast64 = FastCfg<T, 64, 6, sizeof(T) == 4>;  // fp64: plain W plane
 
 template <typename T> using Fast32 = FastCfg<T, 32, 6>;
 // F = 128 (fp32 only: the row-extended W plane is 193 x 128 x 8 B = 198 KB):
@@ -27,7 +27,7 @@ int fast_supported(int dtype, int F, int Mmax, int Nmax, int model_n) {
 
 template <class C, int MODE, bool GUARD>
 static int launch(const FastArgs &a, int grid, int Mmax, int Nmax, int model_n, cudaStream_t s) {
-    const FastLayout L = fast_layout<typename C::T>(C::F, C::NW, Mmax, Nmax, model_n, a.iterations);
+    const FastLayout L = fast_layout<typename C::T>(C::F, C::NW, Mmax, Nmax, model_n, a.iterations, C::EXT);
     auto kern = fse_fast_kernel<C, MODE, GUARD>;
     static thread_local size_t configured = 0;  // largest dynamic smem size set so far
     if (L.total > configured) {
@@ -49,7 +49,7 @@ static int launch(const FastArgs &a, int grid, int Mmax, int Nmax, int model_n, 
 
 template <class C>
 static int launch_redo(const FastArgs &a, int max_entries, int Mmax, int Nmax, int model_n, cudaStream_t s) {
-    const FastLayout L = fast_layout<typename C::T>(C::F, C::NW, Mmax, Nmax, model_n, a.iterations);
+    const FastLayout L = fast_layout<typename C::T>(C::F, C::NW, Mmax, Nmax, model_n, a.iterations, C::EXT);
     auto kern = fse_fast_redo_kernel<C, float>;
     static thread_local size_t configured = 0;
     static thread_local int per_sm = 0, sms = 0;
@@ -72,7 +72,7 @@ static int launch_redo(const FastArgs &a, int max_entries, int Mmax, int Nmax, i
 
 template <class C, typename IT>
 static int launch_dataflow(const FastArgs &a, int Mmax, int Nmax, int model_n, cudaStream_t s) {
-    const FastLayout L = fast_layout<typename C::T>(C::F, C::NW, Mmax, Nmax, model_n, a.iterations);
+    const FastLayout L = fast_layout<typename C::T>(C::F, C::NW, Mmax, Nmax, model_n, a.iterations, C::EXT);
     auto kern = fse_fast_dataflow_kernel<C, IT>;
     static thread_local size_t configured = 0;
     static thread_local int per_sm = 0, sms = 0;
