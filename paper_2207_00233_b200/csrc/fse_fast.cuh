@@ -35,8 +35,9 @@
 
 namespace fse {
 
-template <typename T_, int F_, int NW_, bool EXT_ = true>
+template <typename T_, int F_, int NW_, bool EXT_ = true, int MINB_ = 1>
 struct FastCfg {
+    static constexpr int MINB = MINB_;  // __launch_bounds__ min blocks per SM
     // EXT: row-extended W (rows -F/2..F, no modulo on the gathers).  !EXT: the
     // plain F-row plane with a per-bin wrap select (2/3 of the shared memory;
     // used where the extended plane would cost occupancy, i.e. fp64 at F = 64).
@@ -713,7 +714,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
 }
 
 template <class C, int MODE, bool GUARD>
-__global__ void __launch_bounds__(C::NT) fse_fast_kernel(const FastArgs A, const FastLayout L) {
+__global__ void __launch_bounds__(C::NT, C::MINB) fse_fast_kernel(const FastArgs A, const FastLayout L) {
     extern __shared__ __align__(128) unsigned char sm[];
     fast_window<C, MODE, GUARD, typename C::T>(A, L, blockIdx.x, sm);
 }
