@@ -440,3 +440,32 @@ def test_ragged_and_tiny_frames_fast_path_vs_oracle(shape, B, F, prec):
     else:
         truth = img.astype(np.float64)
         assert abs(psnr(truth, out, mask) - psnr(truth, o_img, mask)) <= FP32_PSNR_DB
+
+
+def test_fp32_guard_redo_everything_matches_fp64():
+    """fse_set_guard(1, 0) hands every fp32 window to the fp64 redo kernel
+    (fse_fast_redo_kernel): the result is the fp64 path's up to fp32 storage of
+    the image (the guard machinery)."""
+    import ctypes
+
+    from paper_2207_00233_b200 import _lib
+
+    img, mask = synth.config_scene(2)
+    img, mask = img[:192, :256].copy(), mask[:192, :256].copy()
+    p = P.FseParams(d=14, iterations=60, block_size=4, fft_size=64)
+    L = _lib.lib()
+    try:
+        L.fse_set_guard(1.0, 0.0)
+        L.fse_guard_redo_count(1)
+        L.fse_timing_enable(1)
+        g32, m32, rep = P.conceal(img, mask, p, precision="fp32")
+        L.fse_timing_enable(0)
+        L.fse_timing_read(None, None, None)
+        redone = int(L.fse_guard_redo_count(1))
+    finally:
+        L.fse_set_guard(-1.0, 0.0)
+        L.fse_timing_enable(0)
+    o64, m64, _ = P.conceal(img, mask, p, precision="fp64")
+    assert redone == rep.blocks_processed
+    np.testing.assert_array_equal(m32, m64)
+    assert np.max(np.abs(g32 - o64)) <= 1e-3
