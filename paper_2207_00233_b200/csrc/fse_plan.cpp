@@ -215,28 +215,40 @@ int build_one(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p, in
         fprintf(stderr, "plan %-12s %.1f ms\n", what, std::chrono::duration<double, std::milli>(now - t_start).count());
         t_start = now;
     };
-    // per-block tallies: lost (grid.py:138-144), usable-as-A, pre-reconstructed
-    std::vector<int32_t> nL(nb, 0), nA(nb, 0), nR0(nb, 0);
-    for (int y = 0; y < H; ++y) {
-        const uint8_t *row = mask + (size_t)y * W;
-        int32_t *L = &nL[(y / B) * cols], *A = &nA[(y / B) * cols], *R0 = &nR0[(y / B) * cols];
-        for (int c = 0; c < cols; ++c) {
-            const int x1 = std::min(W, (c + 1) * B);
-            int32_t l = 0, r0 = 0;
-            for (int x = c * B; x < x1; ++x) {
-                const uint8_t s = row[x];
-                l += s == FSE_LOST;
-                r0 += s == FSE_RECONSTRUCTED;
+    // per-block presence flags (only "any" is ever needed): bit 0 a LOST sample
+    // (lost_per_block > 0, grid.py:138-144), bit 1 a RECONSTRUCTED sample, bit 2
+    // any other state (class A, grid.py:124-130).  Rows are scanned 8 bytes at a
+    // time; all-KNOWN and all-LOST words (the common cases) set one bit of
+    // their blocks without a per-byte pass.
+    std::vector<uint8_t> flag(nb, 0);
+    {
+        uint8_t lut[256];
+        for (int v = 0; v < 256; ++v) lut[v] = v == FSE_LOST ? 1 : (v == FSE_RECONSTRUCTED ? 2 : 4);
+        for (int y = 0; y < H; ++y) {
+            const uint8_t *row = mask + (size_t)y * W;
+            uint8_t *fr = &flag[(size_t)(y / B) * cols];
+            int x = 0;
+            for (; x + 8 <= W; x += 8) {
+                uint64_t w8;
+                std::memcpy(&w8, row + x, 8);
+                if (w8 == 0) {
+                    for (int c = x / B; c <= (x + 7) / B; ++c) fr[c] |= 4;
+                } else if (w8 == 0x0101010101010101ull) {  // a run of LOST samples
+                    for (int c = x / B; c <= (x + 7) / B; ++c) fr[c] |= 1;
+                } else {
+                    for (int i = 0; i < 8; ++i) fr[(x + i) / B] |= lut[row[x + i]];
+                }
             }
-            L[c] += l;
-            R0[c] += r0;
-            A[c] += (x1 - c * B) - l - r0;  // anything else classifies as A (grid.py:124-130)
+            for (; x < W; ++x) fr[x / B] |= lut[row[x]];
         }
     }
+    auto nL = [&](int b) { return (flag[b] & 1) != 0; };
+    auto nR0 = [&](int b) { return (flag[b] & 2) != 0; };
+    auto nA = [&](int b) { return (flag[b] & 4) != 0; };
     std::vector<uint8_t> lossy(nb);
     P.n_lossy = 0;
     for (int b = 0; b < nb; ++b) {
-        lossy[b] = nL[b] > 0;
+        lossy[b] = nL(b);
         P.n_lossy += lossy[b];
     }
     P.max_wr = std::min(H, B + 2 * p->d);
@@ -270,7 +282,7 @@ int build_one(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p, in
     for (int r = 0; r < rows; ++r)
         for (int c = 0; c < cols; ++c) {
             const int o = r * cols + c;
-            const int ok = nA[o] > 0 || (r_counts && nR0[o] > 0);
+            const int ok = nA(o) || (r_counts && nR0(o));
             PS[(size_t)(r + 1) * (cols + 1) + c + 1] = ok + PS[(size_t)r * (cols + 1) + c + 1] +
                                                        PS[(size_t)(r + 1) * (cols + 1) + c] -
                                                        PS[(size_t)r * (cols + 1) + c];
@@ -299,8 +311,8 @@ int build_one(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p, in
                     bool inside = or0 >= wr0 && or1 <= wr1 && oc0 >= wc0 && oc1 <= wc1;
                     if (pass == 0) {
                         if (!inside) continue;
-                        if (nA[o] > 0) return true;
-                        if (r_counts && (nR0[o] > 0 || (written[o] && nL[o] > 0))) return true;
+                        if (nA(o)) return true;
+                        if (r_counts && (nR0(o) || (written[o] && nL(o)))) return true;
                     } else {
                         if (inside) continue;
                         int y0 = std::max(or0, wr0), y1 = std::min(or1, wr1);
