@@ -10,9 +10,12 @@ namespace fse {
 // F = 64: 66 row segments of the half plane over 6 warps -> 11 bins per thread
 // (4 warps / 17 bins measured 5% slower: fewer warps to hide latency).
 // F = 32: 17 row segments over 6 warps -> 3 bins per thread.
-template <typename T> using Fast64 = FastCfg<T, 64, 6, sizeof(T) == 4>;  // fp64: plain W plane
+// min blocks/SM in __launch_bounds__ pins the register budget to the occupancy
+// the shared memory allows (an explicit 1 lets ptxas take 121 registers and
+// halves the fp32 occupancy)
+template <typename T> using Fast64 = FastCfg<T, 64, 6, sizeof(T) == 4, sizeof(T) == 4 ? 4 : 3>;  // fp64: plain W plane
 
-template <typename T> using Fast32 = FastCfg<T, 32, 6>;
+template <typename T> using Fast32 = FastCfg<T, 32, 6, true, 5>;
 // F = 128 (fp32 only: the row-extended W plane is 193 x 128 x 8 B = 198 KB):
 // 260 row segments over 20 warps -> 13 bins per thread, one CTA per SM.
 template <typename T> using Fast128 = FastCfg<T, 128, 20>;
