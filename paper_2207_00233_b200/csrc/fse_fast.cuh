@@ -35,9 +35,9 @@
 
 namespace fse {
 
-template <typename T_, int F_, int NW_, bool EXT_ = true, int MINB_ = 1>
+template <typename T_, int F_, int NW_, bool EXT_ = true, int MINB_ = 0>
 struct FastCfg {
-    static constexpr int MINB = MINB_;  // __launch_bounds__ min blocks per SM
+    static constexpr int MINB = MINB_;  // __launch_bounds__ min blocks per SM (0 = unspecified)
     // EXT: row-extended W (rows -F/2..F, no modulo on the gathers).  !EXT: the
     // plain F-row plane with a per-bin wrap select (2/3 of the shared memory;
     // used where the extended plane would cost occupancy, i.e. fp64 at F = 64).

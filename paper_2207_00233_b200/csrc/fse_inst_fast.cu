@@ -15,7 +15,7 @@ namespace fse {
 // halves the fp32 occupancy)
 template <typename T> using Fast64 = FastCfg<T, 64, 6, sizeof(T) == 4, sizeof(T) == 4 ? 4 : 3>;  // fp64: plain W plane
 
-template <typename T> using Fast32 = FastCfg<T, 32, 6, true, 5>;
+template <typename T> using Fast32 = FastCfg<T, 32, 6>;
 // F = 128 (fp32 only: the row-extended W plane is 193 x 128 x 8 B = 198 KB):
 // 260 row segments over 20 warps -> 13 bins per thread, one CTA per SM.
 template <typename T> using Fast128 = FastCfg<T, 128, 20>;
