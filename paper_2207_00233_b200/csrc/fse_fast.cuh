@@ -74,7 +74,7 @@ struct PickRec {
 };
 
 struct FastLayout {
-    size_t tw, slots, red, model, hist, big, yx, yw, xs, ws, part, total;
+    size_t tw, slots, red, hist, big, yx, yw, xs, ws, part, total;
 };
 
 template <typename T>
@@ -87,7 +87,6 @@ __host__ __device__ inline FastLayout fast_layout(int F, int NW, int Mmax, int N
     o = (o + 15) & ~size_t(15);
     L.slots = o; o += 2 * (size_t)NW * sizeof(FastSlot<double>);
     L.red = o; o += (size_t)(NW + 2) * sizeof(double);
-    L.model = o; o += (size_t)(model_n > 0 ? model_n : 1) * sizeof(T);
     o = (o + 15) & ~size_t(15);
     L.hist = o; o += (size_t)(model_n > 0 ? (iters > 0 ? iters : 1) : 1) * sizeof(PickRec<T>);
     o = (o + 127) & ~size_t(127);

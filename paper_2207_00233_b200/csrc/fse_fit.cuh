@@ -60,14 +60,6 @@ template <typename T> struct Slot {
     T pre, pim;
 };
 
-// Everything a CTA needs to know about its window.
-struct WinGeom {
-    int M, N;        // window rows / cols (samples actually present)
-    int F1, F2;      // DFT size
-    int br0, bc0;    // block rectangle inside the window
-    int bh, bw;
-};
-
 // Shared-memory carve-up, identical on host and device.
 struct SmemLayout {
     size_t tw1, tw2, slots, red, model, big, off_Yx, off_Yw, big_bytes, dbg_res, dbg_w, total;

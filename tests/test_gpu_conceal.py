@@ -446,8 +446,6 @@ def test_fp32_guard_redo_everything_matches_fp64():
     """fse_set_guard(1, 0) hands every fp32 window to the fp64 redo kernel
     (fse_fast_redo_kernel): the result is the fp64 path's up to fp32 storage of
     the image (the guard machinery)."""
-    import ctypes
-
     from paper_2207_00233_b200 import _lib
 
     img, mask = synth.config_scene(2)

@@ -5,7 +5,6 @@ equals the single-process total.  No GPU: plans are host C++ only."""
 import os
 import socket
 
-import numpy as np
 import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp

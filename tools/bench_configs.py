@@ -1,7 +1,6 @@
 """Dev: per-config device timing of the level pipeline (plans prebuilt)."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np
 import torch
 import paper_2207_00233_b200 as P
 from paper_2207_00233_b200 import synth

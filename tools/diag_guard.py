@@ -1,5 +1,5 @@
 """Dev diagnostic: fp32 guard behaviour on golden case 2 (GPU)."""
-import ctypes, sys, os
+import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 import numpy as np

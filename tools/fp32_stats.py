@@ -5,7 +5,7 @@ sys.path[:0] = [R, os.path.join(R, "tests")]
 import numpy as np
 import paper_2207_00233_b200 as P
 from paper_2207_00233_b200 import synth
-from helpers import conceal_case, csr
+from helpers import conceal_case
 
 def psnr(orig, res, mask):
     region = mask != 0
