@@ -31,13 +31,22 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cooperative_groups.h>
+
 #include "fse_kernel.cuh"
 
 namespace fse {
 
-template <typename T_, int F_, int NW_, bool EXT_ = true, int MINB_ = 0>
+template <typename T_, int F_, int NW_, bool EXT_ = true, int MINB_ = 0, int CL_ = 1>
 struct FastCfg {
     static constexpr int MINB = MINB_;  // __launch_bounds__ min blocks per SM (0 = unspecified)
+    // CL > 1: one window is split over a thread-block cluster of CL CTAs (one
+    // per SM): the bins are spread over CL * NW warps, every CTA keeps a full
+    // copy of W, and the per-iteration argmax slots are exchanged through DSMEM
+    // with one cluster barrier.  For dependency levels narrower than the GPU,
+    // where a window's latency, not the throughput, sets the time.
+    static constexpr int CL = CL_;
+    static constexpr int NWT = NW_ * CL_;       // warps per window
     // EXT: row-extended W (rows -F/2..F, no modulo on the gathers).  !EXT: the
     // plain F-row plane with a per-bin wrap select (2/3 of the shared memory;
     // used where the extended plane would cost occupancy, i.e. fp64 at F = 64).
@@ -50,11 +59,12 @@ struct FastCfg {
     static constexpr int R1 = F_ / 2 + 1;       // half-plane rows
     static constexpr int SEG = F_ / 32;         // 32-column segments per row
     static constexpr int NSEGS = R1 * SEG;      // row segments of the half plane
-    static constexpr int NB = (NSEGS + NW_ - 1) / NW_;  // segments (bins) per thread
-    static constexpr int RSTEP = NW_ / SEG;     // row stride between a warp's segments
+    static constexpr int NB = (NSEGS + NWT - 1) / NWT;  // segments (bins) per thread
+    static constexpr int RSTEP = NWT / SEG;     // row stride between a warp's segments
     static constexpr int EXT_ROWS = 3 * F_ / 2 + 1;
     static_assert(F_ == 32 || F_ == 64 || F_ == 128, "fast path: F = 32, 64 or 128");
     static_assert(NW_ % SEG == 0, "NW must be a multiple of F/32");
+    static_assert(NWT <= 32, "one warp reduces the window's slots");
     static_assert(NB <= 32, "5-bit bin tag");
 };
 
@@ -257,9 +267,13 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     using T = typename C::T;
     using T2 = typename C::T2;
     constexpr int F = C::F, NW = C::NW, NT = C::NT, NB = C::NB, R1 = C::R1, SEG = C::SEG;
-    constexpr int RSTEP = C::RSTEP;
+    constexpr int RSTEP = C::RSTEP, CL = C::CL, NWT = C::NWT;
     constexpr bool IS_F32 = sizeof(T) == 4;
+    static_assert(CL == 1 || (MODE == 0 && !GUARD), "clusters: pipeline mode without the guard");
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    int crank = 0;  // rank of this CTA in its cluster
+    if constexpr (CL > 1) crank = (int)cooperative_groups::this_cluster().block_rank();
+    const int gwarp = crank * NW + warp;  // warp index within the window
 
     T2 *tw = reinterpret_cast<T2 *>(sm + L.tw);
     FastSlot<T> *slots = reinterpret_cast<FastSlot<T> *>(sm + L.slots);
@@ -381,10 +395,10 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     }
     __syncthreads();
 
-    // ---- bin ownership: warp w owns row segments w + NW*j: row u0 + RSTEP*j,
-    // columns seg*32 + lane.
-    const int seg = warp % SEG;
-    const int u0 = warp / SEG;
+    // ---- bin ownership: warp w owns row segments w + NWT*j: row u0 + RSTEP*j,
+    // columns seg*32 + lane (w = the warp's index within the window).
+    const int seg = gwarp % SEG;
+    const int u0 = gwarp / SEG;
     const int v = seg * 32 + lane;
 
     // ---- DFT pass 2 (rows), radix-4 over the owners of columns v0 + q F/4:
@@ -448,6 +462,19 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         const int u = u0 + RSTEP * j;
         if (u < R1) Wext[(u + (C::EXT ? F / 2 : 0)) * F + v] = combine(u);
     }
+    if constexpr (CL > 1) {
+        // every CTA of the cluster holds the whole W: fetch the half rows the
+        // other CTAs computed (row u belongs to window warp (u % RSTEP) * SEG)
+        auto cluster = cooperative_groups::this_cluster();
+        cluster.sync();
+        for (int idx = t; idx < R1 * F; idx += NT) {
+            const int u = idx / F;
+            const int owner = ((u % RSTEP) * SEG) / NW;
+            if (owner == crank) continue;
+            T2 *p = Wext + (u + (C::EXT ? F / 2 : 0)) * F + (idx - u * F);
+            *p = *cluster.map_shared_rank(p, owner);
+        }
+    }
     __syncthreads();
     if constexpr (!C::EXT) {
         // plain plane: rows F/2+1 .. F-1 by W[r][c] = conj W[F-r][-c]
@@ -486,7 +513,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
             const int q = lane * NW + warp + k * NT;  // spread over the warps
-            mown[k] = q < bh * bw;
+            mown[k] = q < bh * bw && crank == 0;     // the cluster's CTA 0 writes the block
             if (mown[k]) {
                 mi[k] = br0 + q / bw;
                 mj[k] = bc0 + q % bw;
@@ -536,7 +563,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
 
     for (int it = 0; it < I; ++it) {
         // ---- (1) CTA-wide argmax (+ runner-up for the guard), one barrier
-        FastSlot<T> *sl = slots + (it & 1) * NW;
+        FastSlot<T> *sl = slots + (it & 1) * NWT;
         if constexpr (IS_F32 && GUARD) {
             const unsigned w1 = warp_max_u32(k1);
             const int wl = __ffs(__ballot_sync(0xffffffffu, k1 == w1)) - 1;
@@ -556,13 +583,22 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
             unsigned wlin;
             warp_argmax<T>(key, lin, wkey, wlin);
             if (key == wkey && lin == wlin) {
-                sl[warp].key = wkey;
-                sl[warp].lin = wlin;
-                sl[warp].gre = bg.x;
-                sl[warp].gim = bg.y;
+                FastSlot<T> mine;
+                mine.key = wkey;
+                mine.lin = wlin;
+                mine.gre = bg.x;
+                mine.gim = bg.y;
+                if constexpr (CL > 1) {  // into the slot array of every CTA of the cluster
+                    auto cluster = cooperative_groups::this_cluster();
+#pragma unroll
+                    for (int r = 0; r < CL; ++r) *cluster.map_shared_rank(&sl[gwarp], r) = mine;
+                } else {
+                    sl[gwarp] = mine;
+                }
             }
         }
-        __syncthreads();
+        if constexpr (CL > 1) cooperative_groups::this_cluster().sync();
+        else __syncthreads();
         int a, b, gw;
         if constexpr (IS_F32 && GUARD) {
             const unsigned long long uk = lane < NW ? sl[lane].key : 0ull;
@@ -589,11 +625,14 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
                 }
             }
         } else {
-            const unsigned long long uk = lane < NW ? sl[lane].key : 0ull;
-            const unsigned ul = lane < NW ? sl[lane].lin : 0xFFFFFFFFu;
+            const unsigned long long uk = lane < NWT ? sl[lane].key : 0ull;
+            const unsigned ul = lane < NWT ? sl[lane].lin : 0xFFFFFFFFu;
             unsigned long long gk;
             unsigned glin;
             warp_argmax<T>(uk, ul, gk, glin);
+            // no bin compared greater than -1 (all energies NaN): the reference's
+            // strict-'>' scan keeps its initial pick (0, 0) (_kernel.pyx:32-44)
+            if (glin >= (unsigned)(R1 * F)) glin = 0;
             a = (int)(glin / F);
             b = (int)(glin & (F - 1));
             gw = (a % RSTEP) * SEG + (b >> 5);  // owner warp of bin (a, b)
@@ -611,7 +650,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         const bool selfc = ((2 * a) & (F - 1)) == 0 && ((2 * b) & (F - 1)) == 0;
         // single-thread bookkeeping behind a warp-uniform branch, so the other
         // warps do not issue its predicated stores
-        if (warp == 0 && picks_out) {
+        if (gwarp == 0 && picks_out) {
             if (lane == 0) {
                 picks_out[2 * it] = a;
                 picks_out[2 * it + 1] = b;
@@ -630,7 +669,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
 
         // ---- (2) log the pick for the block model (synthesised after the loop)
         if constexpr (MODE == 0) {
-            if (warp == 0) {
+            if (gwarp == 0) {
                 if (lane == 0) hist[it] = PickRec<T>{a, b, gpr, gpi};
             }
         }
@@ -658,7 +697,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
 #pragma unroll
             for (int q = 0; q < LG; ++q) {
                 const int j = j0 + q;
-                const bool inr = j < NB && ((j < NB - 1) || (C::NSEGS % NW == 0) || (u0 + RSTEP * j < R1));
+                const bool inr = j < NB && ((j < NB - 1) || (C::NSEGS % NWT == 0) || (u0 + RSTEP * j < R1));
                 if (inr) {
                     if constexpr (C::EXT) {
                         wl[q] = lo[j * RSTEP * F];
@@ -672,7 +711,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
 #pragma unroll
             for (int q = 0; q < LG; ++q) {
                 const int j = j0 + q;
-                const bool inr = j < NB && ((j < NB - 1) || (C::NSEGS % NW == 0) || (u0 + RSTEP * j < R1));
+                const bool inr = j < NB && ((j < NB - 1) || (C::NSEGS % NWT == 0) || (u0 + RSTEP * j < R1));
                 if (inr) {
                     G[j] = spectral_update(G[j], wl[q], wh[q], mS, qv);
                     const T e = G[j].x * G[j].x + G[j].y * G[j].y;
@@ -710,12 +749,22 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
                 if (fd->mask[off] == FSE_LOST) img[off] = (IT)mval[k];
             }
     }
+    // keep this CTA's shared memory alive until the cluster is done with it
+    if constexpr (CL > 1) cooperative_groups::this_cluster().sync();
 }
 
 template <class C, int MODE, bool GUARD>
 __global__ void __launch_bounds__(C::NT, C::MINB) fse_fast_kernel(const FastArgs A, const FastLayout L) {
     extern __shared__ __align__(128) unsigned char sm[];
     fast_window<C, MODE, GUARD, typename C::T>(A, L, blockIdx.x, sm);
+}
+
+// Cluster variant: CL CTAs (one window) per cluster, window = blockIdx.x / CL.
+template <class C>
+__global__ void __cluster_dims__(C::CL, 1, 1) __launch_bounds__(C::NT)
+    fse_fast_cluster_kernel(const FastArgs A, const FastLayout L) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    fast_window<C, 0, false, typename C::T>(A, L, blockIdx.x / C::CL, sm);
 }
 
 // Persistent variant over a device-side list (the fp64 redo of guarded windows

@@ -19,6 +19,39 @@ template <typename T> using Fast32 = FastCfg<T, 32, 6>;
 // F = 128 (fp32 only: the row-extended W plane is 193 x 128 x 8 B = 198 KB):
 // 260 row segments over 20 warps -> 13 bins per thread, one CTA per SM.
 template <typename T> using Fast128 = FastCfg<T, 128, 20>;
+// Cluster variants for levels narrower than the GPU: one window over CL SMs.
+template <typename T, int CL> using Fast64C = FastCfg<T, 64, 6, sizeof(T) == 4, 0, CL>;
+template <typename T, int CL> using Fast32C = FastCfg<T, 32, 6, true, 0, CL>;
+
+// FSE_CLUSTER: unset / 0 = off (default), 2 / 4 = that cluster size, -1 = automatic.
+// Off by default: measured slower than one CTA per window even on the narrow
+// levels of configs 1, 2 and 5 (the per-iteration cluster barrier costs more
+// than the shorter bin loop saves).
+static int cluster_mode() {
+    static int v = [] {
+        const char *e = getenv("FSE_CLUSTER");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+bool cluster_levels() { return cluster_mode() != 0; }
+
+template <class C>
+static int launch_cluster(const FastArgs &a, int windows, int Mmax, int Nmax, int model_n, cudaStream_t s) {
+    const FastLayout L = fast_layout<typename C::T>(C::F, C::NWT, Mmax, Nmax, model_n, a.iterations, C::EXT);
+    auto kern = fse_fast_cluster_kernel<C>;
+    static thread_local size_t configured = 0;
+    if (L.total > configured) {
+        FSE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
+        configured = L.total;
+    }
+    if (windows > 0) {
+        kern<<<windows * C::CL, C::NT, L.total, s>>>(a, L);
+        FSE_CUDA_TRY(cudaGetLastError());
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+    return FSE_OK;
+}
 // (A 22-warp / 3-bin "latency" variant for levels narrower than the GPU was
 // measured 20% slower on configs 1-2: per-iteration overhead grows with warps.)
 
@@ -30,7 +63,7 @@ int fast_supported(int dtype, int F, int Mmax, int Nmax, int model_n) {
 
 template <class C, int MODE, bool GUARD>
 static int launch(const FastArgs &a, int grid, int Mmax, int Nmax, int model_n, cudaStream_t s) {
-    const FastLayout L = fast_layout<typename C::T>(C::F, C::NW, Mmax, Nmax, model_n, a.iterations, C::EXT);
+    const FastLayout L = fast_layout<typename C::T>(C::F, C::NWT, Mmax, Nmax, model_n, a.iterations, C::EXT);
     auto kern = fse_fast_kernel<C, MODE, GUARD>;
     static thread_local size_t configured = 0;  // largest dynamic smem size set so far
     if (L.total > configured) {
@@ -52,7 +85,7 @@ static int launch(const FastArgs &a, int grid, int Mmax, int Nmax, int model_n, 
 
 template <class C>
 static int launch_redo(const FastArgs &a, int max_entries, int Mmax, int Nmax, int model_n, cudaStream_t s) {
-    const FastLayout L = fast_layout<typename C::T>(C::F, C::NW, Mmax, Nmax, model_n, a.iterations, C::EXT);
+    const FastLayout L = fast_layout<typename C::T>(C::F, C::NWT, Mmax, Nmax, model_n, a.iterations, C::EXT);
     auto kern = fse_fast_redo_kernel<C, float>;
     static thread_local size_t configured = 0;
     static thread_local int per_sm = 0, sms = 0;
@@ -75,7 +108,7 @@ static int launch_redo(const FastArgs &a, int max_entries, int Mmax, int Nmax, i
 
 template <class C, typename IT>
 static int launch_dataflow(const FastArgs &a, int Mmax, int Nmax, int model_n, cudaStream_t s) {
-    const FastLayout L = fast_layout<typename C::T>(C::F, C::NW, Mmax, Nmax, model_n, a.iterations, C::EXT);
+    const FastLayout L = fast_layout<typename C::T>(C::F, C::NWT, Mmax, Nmax, model_n, a.iterations, C::EXT);
     auto kern = fse_fast_dataflow_kernel<C, IT>;
     static thread_local size_t configured = 0;
     static thread_local int per_sm = 0, sms = 0;
@@ -117,6 +150,31 @@ int fast_dataflow(int dtype, int F, const FastArgs &a, int Mmax, int Nmax, int m
 
 int fast_level(int dtype, int F, bool guard, const FastArgs &a, int grid, int Mmax, int Nmax,
                int model_n, cudaStream_t s) {
+    static const int sms = [] {
+        int dev = 0, v = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+            cudaGetLastError();
+            return 148;
+        }
+        return v;
+    }();
+    // narrow level: give each window 4 (or 2) SMs as a cluster
+    if (!guard && cluster_levels() && (F == 64 || F == 32) && grid * 2 <= sms) {
+        const bool four = cluster_mode() == 4 || (cluster_mode() != 2 && grid * 4 <= sms);
+        if (dtype == FSE_F32) {
+            if (F == 64)
+                return four ? launch_cluster<Fast64C<float, 4>>(a, grid, Mmax, Nmax, model_n, s)
+                            : launch_cluster<Fast64C<float, 2>>(a, grid, Mmax, Nmax, model_n, s);
+            return four ? launch_cluster<Fast32C<float, 4>>(a, grid, Mmax, Nmax, model_n, s)
+                        : launch_cluster<Fast32C<float, 2>>(a, grid, Mmax, Nmax, model_n, s);
+        }
+        if (F == 64)
+            return four ? launch_cluster<Fast64C<double, 4>>(a, grid, Mmax, Nmax, model_n, s)
+                        : launch_cluster<Fast64C<double, 2>>(a, grid, Mmax, Nmax, model_n, s);
+        return four ? launch_cluster<Fast32C<double, 4>>(a, grid, Mmax, Nmax, model_n, s)
+                    : launch_cluster<Fast32C<double, 2>>(a, grid, Mmax, Nmax, model_n, s);
+    }
     if (dtype == FSE_F32) {
         if (F == 128) return launch<Fast128<float>, 0, false>(a, grid, Mmax, Nmax, model_n, s);
         if (F == 64)
