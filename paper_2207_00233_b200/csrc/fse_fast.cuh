@@ -322,28 +322,59 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     // ---- staging: classes -> weights (fse.py:105-119); x = w * select(w > 0, v, 0)
     double wsum = 0.0;
     if constexpr (MODE == 0) {
+        // a warp stages window rows (lane = column: coalesced mask / image
+        // reads, no index division); the global loads of RB rows are issued
+        // before any of their math so their latencies overlap
         const int myrank = fd->rank[blk];
         const IT *img = reinterpret_cast<const IT *>(fd->image);
-        for (int idx = t; idx < M * N; idx += NT) {
-            const int i = idx / N, j = idx - i * N;
-            const int y = wr0 + i, x = wc0 + j;
-            const uint8_t s = fd->mask[(size_t)y * A.W + x];
-            const double dec = A.decay[abs(2 * i - (M - 1)) * A.decay_dim + abs(2 * j - (N - 1))];
-            double w;
-            if (s == FSE_LOST) {
-                const int owner = (y / A.B) * A.cols + x / A.B;
-                // R iff the owner block was written by an earlier batch
-                // (snapshot semantics, conceal.py:148-163); BI/BO otherwise
-                w = (owner != blk && fd->rank[owner] < myrank) ? A.delta * dec : 0.0;
-            } else if (s == FSE_RECONSTRUCTED) {
-                w = A.delta * dec;
-            } else {
-                w = dec;
+        const uint8_t *msk = fd->mask;
+        const int32_t *rnk = fd->rank;
+        constexpr int RB = 4;
+        for (int jc = 0; jc < N; jc += 32) {
+            const int j = jc + lane;
+            const bool jin = j < N;
+            const int x = wc0 + (jin ? j : 0);
+            const int bx = x / A.B;
+            const int dj = abs(2 * j - (N - 1));
+            for (int i0 = warp; i0 < M; i0 += NW * RB) {
+                uint8_t s[RB];
+                IT val[RB];
+                int32_t orank[RB], owner[RB];
+                double dec[RB];
+#pragma unroll
+                for (int r = 0; r < RB; ++r) {
+                    const int i = i0 + r * NW;
+                    if (jin && i < M) {
+                        const int y = wr0 + i;
+                        const size_t off = (size_t)y * A.W + x;
+                        owner[r] = (y / A.B) * A.cols + bx;
+                        s[r] = msk[off];
+                        val[r] = img[off];
+                        orank[r] = rnk[owner[r]];
+                        dec[r] = A.decay[abs(2 * i - (M - 1)) * A.decay_dim + dj];
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < RB; ++r) {
+                    const int i = i0 + r * NW;
+                    if (jin && i < M) {
+                        double w;
+                        if (s[r] == FSE_LOST) {
+                            // R iff the owner block was written by an earlier batch
+                            // (snapshot semantics, conceal.py:148-163); BI/BO otherwise
+                            w = (owner[r] != blk && orank[r] < myrank) ? A.delta * dec[r] : 0.0;
+                        } else if (s[r] == FSE_RECONSTRUCTED) {
+                            w = A.delta * dec[r];
+                        } else {
+                            w = dec[r];
+                        }
+                        const double v = (double)val[r];
+                        xs[i * N + j] = w > 0.0 ? (T)(w * v) : (T)0;
+                        ws[i * N + j] = (T)w;
+                        wsum += w;
+                    }
+                }
             }
-            const double v = (double)img[(size_t)y * A.W + x];
-            xs[idx] = w > 0.0 ? (T)(w * v) : (T)0;
-            ws[idx] = (T)w;
-            wsum += w;
         }
     } else {
         const T *val = reinterpret_cast<const T *>(A.values) + (size_t)entry_idx * M * N;
@@ -409,6 +440,13 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     // bins; W goes to registers first, to the ext rows once `part` is dead.
     constexpr int QW = F / 4;
     const int q4 = v / QW, v0 = v - q4 * QW;
+    // the twiddle sequence e^{-j 2 pi v0 n / F}, n = q4 + 4 i, is the same for
+    // every row: its first NR terms (n < 4 NR) stay in registers
+    constexpr int NR = IS_F32 ? 8 : 4;
+    const int tstep = (4 * v0) & (F - 1);
+    T2 twr[NR];
+#pragma unroll
+    for (int i = 0; i < NR; ++i) twr[i] = tw[(v0 * q4 + tstep * i) & (F - 1)];
     auto partials = [&](const T2 *Y) {
 #pragma unroll
         for (int j = 0; j < NB; ++j) {
@@ -416,11 +454,13 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
             if (u < R1) {
                 const T2 *yr = Y + u * N;
                 T2 acc = T2{0, 0};
-                int k = (v0 * q4) & (F - 1);
-                const int step = (4 * v0) & (F - 1);
-                for (int n = q4; n < N; n += 4) {
+#pragma unroll
+                for (int i = 0; i < NR; ++i)
+                    if (q4 + 4 * i < N) acc = dft_mac(acc, yr[q4 + 4 * i], twr[i]);
+                int k = (v0 * q4 + tstep * NR) & (F - 1);
+                for (int n = q4 + 4 * NR; n < N; n += 4) {
                     acc = dft_mac(acc, yr[n], tw[k]);
-                    k = (k + step) & (F - 1);
+                    k = (k + tstep) & (F - 1);
                 }
                 part[(u * 4 + q4) * QW + v0] = acc;
             }
