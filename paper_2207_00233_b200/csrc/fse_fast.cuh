@@ -76,9 +76,26 @@ struct FastSlot {
     T gre, gim;              // g of the warp's best bin
 };
 
+// A warp's argmax candidate (exact energy key, row-major bin index, g); one
+// 16-byte store for fp32.
+template <typename T>
+struct ArgSlot;
+template <>
+struct __align__(16) ArgSlot<float> {
+    unsigned key, lin;
+    float gre, gim;
+};
+template <>
+struct __align__(16) ArgSlot<double> {
+    unsigned long long key;
+    unsigned lin, pad;
+    double gre, gim;
+};
+static_assert(sizeof(ArgSlot<double>) <= sizeof(FastSlot<double>), "slot region");
+
 // One iteration's contribution to the block model: pick (a, b) and gamma*p.
 template <typename T>
-struct PickRec {
+struct __align__(16) PickRec {
     int a, b;
     T gpr, gpi;
 };
@@ -175,36 +192,27 @@ struct FastArgs {
 __device__ __forceinline__ unsigned warp_max_u32(unsigned v) { return __reduce_max_sync(0xffffffffu, v); }
 __device__ __forceinline__ unsigned warp_min_u32(unsigned v) { return __reduce_min_sync(0xffffffffu, v); }
 
-// Order-preserving unsigned images of IEEE values (for integer REDUX).
-__device__ __forceinline__ unsigned long long ord_key(float e) {
-    const unsigned b = __float_as_uint(e);
-    return (int)b >= 0 ? (b | 0x80000000u) : ~b;
-}
-__device__ __forceinline__ unsigned long long ord_key(double e) {
-    const unsigned long long b = (unsigned long long)__double_as_longlong(e);
-    return (long long)b >= 0 ? (b | 0x8000000000000000ull) : ~b;
+// Keys of non-negative energies for integer REDUX: the IEEE bits of a value
+// >= 0 order like the value.
+__device__ __forceinline__ unsigned energy_key(float e) { return __float_as_uint(e); }
+__device__ __forceinline__ unsigned long long energy_key(double e) {
+    return (unsigned long long)__double_as_longlong(e);
 }
 
 // Warp argmax of (key, lin): largest key, ties to the smallest lin (the
 // reference's first maximum in row-major order, _kernel.pyx:32-44).  Returns
 // the winning key and lin, uniform across the warp.
-template <typename T>
+__device__ __forceinline__ void warp_argmax(unsigned key, unsigned lin, unsigned &wkey, unsigned &wlin) {
+    wkey = warp_max_u32(key);
+    wlin = warp_min_u32(key == wkey ? lin : 0xFFFFFFFFu);
+}
 __device__ __forceinline__ void warp_argmax(unsigned long long key, unsigned lin, unsigned long long &wkey,
                                             unsigned &wlin) {
-    bool match;
-    if constexpr (sizeof(T) == 4) {
-        const unsigned k = (unsigned)key;
-        const unsigned m = warp_max_u32(k);
-        match = k == m;
-        wkey = m;
-    } else {
-        const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
-        const unsigned mh = warp_max_u32(hi);
-        const unsigned ml = warp_max_u32(hi == mh ? lo : 0u);
-        match = hi == mh && lo == ml;
-        wkey = ((unsigned long long)mh << 32) | ml;
-    }
-    wlin = warp_min_u32(match ? lin : 0xFFFFFFFFu);
+    const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+    const unsigned mh = warp_max_u32(hi);
+    const unsigned ml = warp_max_u32(hi == mh ? lo : 0u);
+    wkey = ((unsigned long long)mh << 32) | ml;
+    wlin = warp_min_u32(hi == mh && lo == ml ? lin : 0xFFFFFFFFu);
 }
 
 // ---- complex pair arithmetic.  fp32 uses the sm_100 packed f32x2 pipe
@@ -252,6 +260,14 @@ __device__ __forceinline__ T2 spectral_update(T2 g, T2 lo, T2 hi, T2 mS, T2 qv) 
     const T2 S = cadd(lo, hi), D = csub(lo, hi);
     g = cfma(mS, S, g);
     return cfma(qv, T2{D.y, D.x}, g);
+}
+
+// fp32 form with both FFMA2 multipliers as scalar broadcasts (-gpr, gpi): the
+// sign of the imaginary term moves onto the swizzled difference operand
+__device__ __forceinline__ float2 spectral_update_bc(float2 g, float2 lo, float2 hi, float ngpr, float gpi) {
+    const float2 S = cadd(lo, hi), D = csub(lo, hi);
+    g = cfma(float2{ngpr, ngpr}, S, g);
+    return cfma(float2{gpi, gpi}, float2{D.y, -D.x}, g);
 }
 
 // acc += z * e^{-j theta}, tw = (cos theta, sin theta): the forward-DFT MAC
@@ -398,30 +414,53 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     // x is real, so with even/odd partial sums Ee, Eo over m:
     //   Y[k1] = Ee + Eo,  Y[F/2 - k1] = conj(Ee - Eo)    (e^{-j pi m} = (-1)^m)
     // and only k1 <= F/4 is summed.
-    for (int o = t; o < (F / 4 + 1) * N; o += NT) {
-        const int k1 = o / N, n = o - k1 * N;
-        T2 Xe = T2{0, 0}, Xo = T2{0, 0}, We = T2{0, 0}, Wo = T2{0, 0};
-        int k = 0;
-        for (int m = 0; m < M; m += 2) {
-            const T2 tv = tw[k];
-            const T xv = xs[m * N + n], wv = ws[m * N + n];
-            Xe = cfma(T2{xv, -xv}, tv, Xe);  // x e^{-j theta}
-            We = cfma(T2{wv, -wv}, tv, We);
-            k = (k + k1) & (F - 1);
-            if (m + 1 < M) {
-                const T2 tu = tw[k];
-                const T xu = xs[(m + 1) * N + n], wu = ws[(m + 1) * N + n];
-                Xo = cfma(T2{xu, -xu}, tu, Xo);
-                Wo = cfma(T2{wu, -wu}, tu, Wo);
+    // Lanes take columns n (conflict-free sample reads), warps take k1 = warp +
+    // NW r, so one read of x[m][n], w[m][n] feeds KR outputs; the twiddle
+    // index is warp-uniform (broadcast read).
+    {
+        constexpr int K1N = F / 4 + 1, KR = (K1N + NW - 1) / NW;
+        for (int nc = 0; nc < N; nc += 32) {
+            const int n = nc + lane;
+            if (n < N) {
+                T2 Xe[KR], Xo[KR], We[KR], Wo[KR];
+                int kk[KR];
+#pragma unroll
+                for (int r = 0; r < KR; ++r) {
+                    Xe[r] = Xo[r] = We[r] = Wo[r] = T2{0, 0};
+                    kk[r] = 0;
+                }
+                for (int m = 0; m < M; m += 2) {
+                    const T xv = xs[m * N + n], wv = ws[m * N + n];
+                    const bool odd = m + 1 < M;
+                    const T xu = odd ? xs[(m + 1) * N + n] : (T)0, wu = odd ? ws[(m + 1) * N + n] : (T)0;
+#pragma unroll
+                    for (int r = 0; r < KR; ++r) {
+                        const int k1 = warp + NW * r;
+                        if (k1 < K1N) {
+                            const T2 tv = tw[kk[r]];
+                            Xe[r] = cfma(T2{xv, -xv}, tv, Xe[r]);  // x e^{-j theta}
+                            We[r] = cfma(T2{wv, -wv}, tv, We[r]);
+                            const T2 tu = tw[(kk[r] + k1) & (F - 1)];
+                            Xo[r] = cfma(T2{xu, -xu}, tu, Xo[r]);
+                            Wo[r] = cfma(T2{wu, -wu}, tu, Wo[r]);
+                            kk[r] = (kk[r] + 2 * k1) & (F - 1);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < KR; ++r) {
+                    const int k1 = warp + NW * r;
+                    if (k1 < K1N) {
+                        Yx[k1 * N + n] = cadd(Xe[r], Xo[r]);
+                        Yw[k1 * N + n] = cadd(We[r], Wo[r]);
+                        if (k1 != F / 4) {
+                            const T2 dx = csub(Xe[r], Xo[r]), dw = csub(We[r], Wo[r]);
+                            Yx[(F / 2 - k1) * N + n] = T2{dx.x, -dx.y};
+                            Yw[(F / 2 - k1) * N + n] = T2{dw.x, -dw.y};
+                        }
+                    }
+                }
             }
-            k = (k + k1) & (F - 1);
-        }
-        Yx[k1 * N + n] = cadd(Xe, Xo);
-        Yw[k1 * N + n] = cadd(We, Wo);
-        if (k1 != F / 4) {
-            const T2 dx = csub(Xe, Xo), dw = csub(We, Wo);
-            Yx[(F / 2 - k1) * N + n] = T2{dx.x, -dx.y};
-            Yw[(F / 2 - k1) * N + n] = T2{dw.x, -dw.y};
         }
     }
     __syncthreads();
@@ -574,13 +613,17 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     }
 
     // ---- per-thread argmax state over the owned bins
-    // fp32: packed 32-bit keys (energy bits with a 4-bit bin tag, larger =
-    // better, smaller j wins ties), top-2 for the guard.  fp64: exact energy.
+    // fp32 guard: packed 32-bit keys (energy bits with a 5-bit bin tag, larger =
+    // better, smaller j wins ties) and the runner-up.  Otherwise the exact
+    // energy with the row-major index of its bin.  Energies are >= 0, so their
+    // IEEE bits order like the values, and starting from 0 with no bin is the
+    // reference's strict-'>' scan from -1 up to its all-zero case (below).
     unsigned k1 = 0, k2 = 0;
     // (two interleaved even/odd running maxima were measured 4% slower: more
     // registers and moves than the serial compare chain costs)
-    T best = (T)-1;
-    int bj = -1;
+    T best = (T)0;
+    unsigned blin = 0xFFFFFFFFu;       // row-major index of the best bin, none yet
+    const unsigned lin0 = (unsigned)(u0 * F + v);
     T2 bg = T2{0, 0};  // g of the best bin, carried along (no register indexing later)
     auto track = [&](int j, T e) {
         if constexpr (IS_F32 && GUARD) {
@@ -591,7 +634,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         } else {
             if (e > best) {
                 best = e;
-                bj = j;
+                blin = lin0 + (unsigned)(j * RSTEP * F);
                 bg = G[j];
             }
         }
@@ -601,9 +644,14 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     for (int j = 0; j < NB; ++j)
         if ((valid >> j) & 1u) track(j, G[j].x * G[j].x + G[j].y * G[j].y);
 
+    // fp32: gamma / sum(w) folded into one factor (gamma = 0.5 keeps the
+    // products bit-identical); MODE 1 logs p itself
+    const T ginv = gamma * inv_tot;
+    ArgSlot<T> *asl0 = reinterpret_cast<ArgSlot<T> *>(slots);
     for (int it = 0; it < I; ++it) {
         // ---- (1) CTA-wide argmax (+ runner-up for the guard), one barrier
         FastSlot<T> *sl = slots + (it & 1) * NWT;
+        ArgSlot<T> *asl = asl0 + (it & 1) * NWT;
         if constexpr (IS_F32 && GUARD) {
             const unsigned w1 = warp_max_u32(k1);
             const int wl = __ffs(__ballot_sync(0xffffffffu, k1 == w1)) - 1;
@@ -617,13 +665,14 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
                 sl[warp].gim = bg.y;
             }
         } else {
-            const unsigned lin = bj >= 0 ? (unsigned)((u0 + RSTEP * bj) * F + v) : 0xFFFFFFFFu;
-            const unsigned long long key = ord_key(best);
-            unsigned long long wkey;
+            const auto key = energy_key(best);
+            decltype(energy_key(best)) wkey;
             unsigned wlin;
-            warp_argmax<T>(key, lin, wkey, wlin);
-            if (key == wkey && lin == wlin) {
-                FastSlot<T> mine;
+            warp_argmax(key, blin, wkey, wlin);
+            // one writer: the lane of the warp's first maximum (all lanes when
+            // the warp has no bin above 0; they all hold the same empty slot)
+            if (key == wkey && blin == wlin) {
+                ArgSlot<T> mine;
                 mine.key = wkey;
                 mine.lin = wlin;
                 mine.gre = bg.x;
@@ -631,19 +680,20 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
                 if constexpr (CL > 1) {  // into the slot array of every CTA of the cluster
                     auto cluster = cooperative_groups::this_cluster();
 #pragma unroll
-                    for (int r = 0; r < CL; ++r) *cluster.map_shared_rank(&sl[gwarp], r) = mine;
+                    for (int r = 0; r < CL; ++r) *cluster.map_shared_rank(&asl[gwarp], r) = mine;
                 } else {
-                    sl[gwarp] = mine;
+                    asl[gwarp] = mine;
                 }
             }
         }
         if constexpr (CL > 1) cooperative_groups::this_cluster().sync();
         else __syncthreads();
-        int a, b, gw;
+        int a, b;
+        T2 gwin;
         if constexpr (IS_F32 && GUARD) {
             const unsigned long long uk = lane < NW ? sl[lane].key : 0ull;
             const unsigned long long gk = warp_max_key(uk);
-            gw = __ffs(__ballot_sync(0xffffffffu, uk == gk)) - 1;
+            const int gw = __ffs(__ballot_sync(0xffffffffu, uk == gk)) - 1;
             const int lin = (int)(0xFFFFFFFFu - (unsigned)(gk & 0xFFFFFFFFull));
             a = lin / F;
             b = lin - a * F;
@@ -664,44 +714,47 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
                     return;
                 }
             }
+            gwin = *reinterpret_cast<const T2 *>(&sl[gw].gre);
         } else {
-            const unsigned long long uk = lane < NWT ? sl[lane].key : 0ull;
-            const unsigned ul = lane < NWT ? sl[lane].lin : 0xFFFFFFFFu;
-            unsigned long long gk;
+            const bool in = lane < NWT;
+            const auto uk = in ? asl[lane].key : decltype(asl[0].key)(0);
+            const unsigned ul = in ? asl[lane].lin : 0xFFFFFFFFu;
+            decltype(asl[0].key) gk;
             unsigned glin;
-            warp_argmax<T>(uk, ul, gk, glin);
-            // no bin compared greater than -1 (all energies NaN): the reference's
-            // strict-'>' scan keeps its initial pick (0, 0) (_kernel.pyx:32-44)
+            warp_argmax(uk, ul, gk, glin);
+            // the winning slot (any slot when no bin is above 0: all hold g = 0)
+            const int gw = __ffs(__ballot_sync(0xffffffffu, in && ul == glin)) - 1;
+            // no bin above 0 (all energies 0 or NaN): the reference's strict-'>'
+            // scan from -1 keeps (0, 0) (_kernel.pyx:32-44), whose g is 0
             if (glin >= (unsigned)(R1 * F)) glin = 0;
             a = (int)(glin / F);
             b = (int)(glin & (F - 1));
-            gw = (a % RSTEP) * SEG + (b >> 5);  // owner warp of bin (a, b)
+            gwin = T2{asl[gw].gre, asl[gw].gim};
         }
         // p = g[a,b] / sum(w) (_kernel.pyx:46-47); fp32 multiplies by 1/sum(w)
-        T pre, pim;
-        const T2 gwin = *reinterpret_cast<const T2 *>(&sl[gw].gre);
-        if constexpr (IS_F32) {
-            pre = gwin.x * inv_tot;
-            pim = gwin.y * inv_tot;
-        } else {
-            pre = gwin.x / tot;
-            pim = gwin.y / tot;
-        }
         const bool selfc = ((2 * a) & (F - 1)) == 0 && ((2 * b) & (F - 1)) == 0;
-        // single-thread bookkeeping behind a warp-uniform branch, so the other
-        // warps do not issue its predicated stores
-        if (gwarp == 0 && picks_out) {
-            if (lane == 0) {
+        T gpr, gpi;
+        if constexpr (IS_F32) {
+            gpr = gwin.x * ginv;
+            gpi = gwin.y * ginv;
+        } else {
+            gpr = gamma * (gwin.x / tot);
+            gpi = gamma * (gwin.y / tot);
+        }
+        if constexpr (MODE == 1) {
+            if (gwarp == 0 && lane == 0) {
                 picks_out[2 * it] = a;
                 picks_out[2 * it + 1] = b;
-                if constexpr (MODE == 1) {
-                    plog[2 * it] = pre;
-                    plog[2 * it + 1] = pim;
+                if constexpr (IS_F32) {
+                    plog[2 * it] = gwin.x * inv_tot;
+                    plog[2 * it + 1] = gwin.y * inv_tot;
+                } else {
+                    plog[2 * it] = gwin.x / tot;
+                    plog[2 * it + 1] = gwin.y / tot;
                 }
             }
         }
         // self-conjugate: gamma * Re(p) * W[k - j] == (gamma Re(p) / 2) (W[k-j] + W[k+j])
-        T gpr = gamma * pre, gpi = gamma * pim;
         if (selfc) {
             gpr = gpr * (T)0.5;
             gpi = (T)0;
@@ -709,9 +762,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
 
         // ---- (2) log the pick for the block model (synthesised after the loop)
         if constexpr (MODE == 0) {
-            if (gwarp == 0) {
-                if (lane == 0) hist[it] = PickRec<T>{a, b, gpr, gpi};
-            }
+            if (gwarp == 0 && lane == 0) hist[it] = PickRec<T>{a, b, gpr, gpi};
         }
         if (it + 1 == I) break;  // the last spectrum update is never observed
 
@@ -726,8 +777,8 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         const T2 *loW = lo + F * F, *hiW = hi - F * F;  // plain plane: wrapped bases
         k1 = 0;
         k2 = 0;
-        best = (T)-1;
-        bj = -1;
+        best = (T)0;
+        blin = 0xFFFFFFFFu;
         const T2 mS = T2{-gpr, -gpr}, qv = T2{gpi, -gpi};
         // loads of a group of LG bins are issued before its math (smem latency)
         constexpr int LG = IS_F32 ? 4 : 2;
@@ -753,7 +804,8 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
                 const int j = j0 + q;
                 const bool inr = j < NB && ((j < NB - 1) || (C::NSEGS % NWT == 0) || (u0 + RSTEP * j < R1));
                 if (inr) {
-                    G[j] = spectral_update(G[j], wl[q], wh[q], mS, qv);
+                    if constexpr (IS_F32) G[j] = spectral_update_bc(G[j], wl[q], wh[q], -gpr, gpi);
+                    else G[j] = spectral_update(G[j], wl[q], wh[q], mS, qv);
                     const T e = G[j].x * G[j].x + G[j].y * G[j].y;
                     if (j == 0 || j == NB - 1) {
                         if ((valid >> j) & 1u) track(j, e);
@@ -769,6 +821,11 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     // fse.py:159 restricted to the block rect, accumulated in iteration order
     if constexpr (MODE == 0) {
         __syncthreads();
+        if (picks_out && crank == 0)
+            for (int i = t; i < I; i += NT) {
+                picks_out[2 * i] = hist[i].a;
+                picks_out[2 * i + 1] = hist[i].b;
+            }
 #pragma unroll
         for (int k = 0; k < 2; ++k)
             if (mown[k])
