@@ -10,7 +10,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfse_b200.so")
+LIB_PATH = os.environ.get("FSE_LIB") or os.path.join(_HERE, "libfse_b200.so")
 
 FSE_OK, FSE_EINVAL, FSE_ENOMEM, FSE_ECUDA, FSE_ENOTSUP = 0, -22, -12, -5, -95
 FSE_F64, FSE_F32 = 0, 1

@@ -21,6 +21,12 @@ REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(REPO, "build", "fse_b200")
 LIB = os.path.join(PKG, "libfse_b200.so")
+# dev A/B builds: FSE_BUILD_TAG=x FSE_NVCC_DEFS="-DFOO" builds variants/libfse_b200_x.so
+# (own object dir); load one with FSE_LIB=<path>.  The product build ignores both.
+_TAG = os.environ.get("FSE_BUILD_TAG", "")
+if _TAG:
+    OBJ = os.path.join(REPO, "build", "fse_b200_" + _TAG)
+    LIB = os.path.join(PKG, "variants", f"libfse_b200_{_TAG}.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
               "--expt-relaxed-constexpr"]
@@ -57,6 +63,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(o)
         if force or _stale(o, [s] + hdrs):
             cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-I", os.path.join(REPO, "include"), "-c", s, "-o", o]
+            if _TAG:
+                cmd += os.environ.get("FSE_NVCC_DEFS", "").split()
             if src.endswith(".cu"):
                 cmd += ["-Xptxas", "-v"] if verbose else []
             jobs.append(cmd)
@@ -71,6 +79,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
         list(ex.map(run, jobs))
+    os.makedirs(os.path.dirname(LIB), exist_ok=True)
     if force or jobs or _stale(LIB, objs):
         run([nvcc, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs])
     return LIB

@@ -144,7 +144,7 @@ __host__ __device__ inline FastLayout fast_layout(int F, int NW, int Mmax, int N
         // plain plane: half rows 0..F/2 at [0, HEc); partials above both the
         // Y planes (read by the partials) and the half rows (written by the
         // w combine); xs / ws are dead once the partials start
-        const size_t HEc = (size_t)(F / 2 + 1) * F * c2, FULL = (size_t)F * F * c2;
+        const size_t HEc = (size_t)(F / 2 + 1) * F * c2, FULL = (size_t)(F + 1) * F * c2;
         L.part = 2 * yb > HEc ? 2 * yb : HEc;
         bigb = L.part + pb;
         if (bigb < L.ws + xb) bigb = L.ws + xb;
@@ -267,7 +267,7 @@ __device__ __forceinline__ T2 spectral_update(T2 g, T2 lo, T2 hi, T2 mS, T2 qv) 
 __device__ __forceinline__ float2 spectral_update_bc(float2 g, float2 lo, float2 hi, float ngpr, float gpi) {
     const float2 S = cadd(lo, hi), D = csub(lo, hi);
     g = cfma(float2{ngpr, ngpr}, S, g);
-    return cfma(float2{gpi, gpi}, float2{D.y, -D.x}, g);
+    return cfma(float2{D.y, -D.x}, float2{gpi, gpi}, g);
 }
 
 // acc += z * e^{-j theta}, tw = (cos theta, sin theta): the forward-DFT MAC
@@ -556,11 +556,12 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     }
     __syncthreads();
     if constexpr (!C::EXT) {
-        // plain plane: rows F/2+1 .. F-1 by W[r][c] = conj W[F-r][-c]
-        for (int idx = t; idx < (F / 2 - 1) * F; idx += NT) {
+        // plain plane: rows F/2+1 .. F-1 by W[r][c] = conj W[F-r][-c], and
+        // row F = row 0 (the update's row u + a <= F then never wraps)
+        for (int idx = t; idx < (F / 2) * F; idx += NT) {
             const int rr = F / 2 + 1 + idx / F, c = idx % F;
-            const T2 src = Wext[(F - rr) * F + ((F - c) & (F - 1))];
-            Wext[rr * F + c] = T2{src.x, -src.y};
+            const T2 src = Wext[((F - rr) & (F - 1)) * F + (rr == F ? c : (F - c) & (F - 1))];
+            Wext[rr * F + c] = rr == F ? src : T2{src.x, -src.y};
         }
     }
     // extension rows: W[-s] = conj W[s] reflected, W[F] = W[0]
@@ -769,12 +770,13 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         // ---- (3) spectrum update by the shifted weight spectrum + next argmax
         const int cm = (v - b) & (F - 1), cp = (v + b) & (F - 1);
         // EXT: rows u-a and u+a are in the extended plane as they are.
-        // plain: row (u0 - a + RSTEP j) mod F wraps once over the j range (below
-        // 0), row (u0 + a + RSTEP j) wraps only at F; pick the base per j.
+        // plain: row (u0 - a + RSTEP j) mod F wraps for the first jl bins (below
+        // 0); row u0 + a + RSTEP j <= F is stored as it is (row F = row 0).
         const int x0 = u0 - a, y0 = u0 + a;
         const T2 *lo = Wext + (C::EXT ? (x0 + F / 2) * F : x0 * F) + cm;
         const T2 *hi = Wext + (C::EXT ? (y0 + F / 2) * F : y0 * F) + cp;
-        const T2 *loW = lo + F * F, *hiW = hi - F * F;  // plain plane: wrapped bases
+        const T2 *loW = lo + F * F;  // plain plane: wrapped base
+        const int jl = x0 < 0 ? (RSTEP - 1 - x0) / RSTEP : 0;
         k1 = 0;
         k2 = 0;
         best = (T)0;
@@ -794,8 +796,8 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
                         wl[q] = lo[j * RSTEP * F];
                         wh[q] = hi[j * RSTEP * F];
                     } else {
-                        wl[q] = (x0 + RSTEP * j < 0 ? loW : lo)[j * RSTEP * F];
-                        wh[q] = (y0 + RSTEP * j >= F ? hiW : hi)[j * RSTEP * F];
+                        wl[q] = (j < jl ? loW : lo)[j * RSTEP * F];
+                        wh[q] = hi[j * RSTEP * F];
                     }
                 }
             }
