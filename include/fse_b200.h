@@ -156,6 +156,12 @@ int fse_set_guard(double tau0, double tau1);
  * when their own inputs are written), 0 (default) = one launch per dependency
  * level.  Results are identical.  Process-wide; FSE_DATAFLOW=1 sets the default. */
 int fse_set_dataflow(int32_t on);
+/* Frame groups of one fse_conceal_frames call (level-launch mode): the frames
+ * are split into n contiguous groups of about equal work whose level sequences
+ * run on forked streams, so one group's partial last wave of a level overlaps
+ * another group's work.  1..8, default 2 (FSE_GROUPS sets the default).
+ * Results are identical for every n.  Process-wide. */
+int fse_set_groups(int32_t n);
 /* Windows redone in fp64 by the guard, summed over timed calls (fse_timing_*). */
 int64_t fse_guard_redo_count(int32_t reset);
 

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -39,6 +40,29 @@ static bool g_dataflow = [] {
     return e && e[0] == '1';
 }();
 bool dataflow_enabled() { return g_dataflow; }
+
+// Frame groups of one fse_conceal_frames call run their level sequences on
+// separate forked streams, so the partial last wave of one group's level
+// overlaps the next level of another (the levels of different frames are
+// independent).  FSE_GROUPS=1 restores one launch sequence.
+static int g_groups = [] {
+    const char *e = getenv("FSE_GROUPS");
+    const int v = e ? atoi(e) : 2;
+    return std::max(1, std::min(v, 8));
+}();
+
+// Per-device pool of non-blocking streams for the groups (created once).
+static cudaStream_t group_stream(int g) {
+    constexpr int MAXD = 16, MAXG = 8;
+    static cudaStream_t pool[MAXD][MAXG] = {};
+    static std::mutex mu;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= MAXD || g < 0 || g >= MAXG) return nullptr;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!pool[dev][g]) cudaStreamCreateWithFlags(&pool[dev][g], cudaStreamNonBlocking);
+    return pool[dev][g];
+}
 static long long g_redo_total = 0;
 
 // FP32 FMA throughput probe: 8 independent FFMA chains per thread.
@@ -257,6 +281,12 @@ int fse_set_dataflow(int32_t on) {
     return FSE_OK;
 }
 
+int fse_set_groups(int32_t n) {
+    if (n < 1 || n > 8) return fail(FSE_EINVAL, "groups must be 1..8");
+    fse::g_groups = n;
+    return FSE_OK;
+}
+
 int64_t fse_guard_redo_count(int32_t reset) {
     const long long v = fse::g_redo_total;
     if (reset) fse::g_redo_total = 0;
@@ -324,9 +354,9 @@ int fse_run_windows(int32_t n, int32_t M, int32_t N, int32_t F1, int32_t F2, con
 struct FseShard {
     int n = 0, H = 0, W = 0, B = 0, d = 0, rows = 0, cols = 0, nb = 0, R = 0;
     int dtype = 0, F1 = 0, F2 = 0, Mmax = 0, Nmax = 0, model_n = 0;
-    int row_lo = 0, row_hi = 0, n_levels = 0;
+    int row_lo = 0, row_hi = 0, n_levels = 0, groups = 1;
     size_t n_entries = 0;
-    std::vector<int> lvl_off;
+    std::vector<int> lvl_off;  // entry offset of (group g, level l) at g * n_levels + l
     std::vector<int32_t> edge;  // per level: bit0 top zone, bit1 bottom zone touched
     unsigned char *dev = nullptr;
     size_t off_ent = 0, off_cnt = 0, off_next = 0, off_done = 0, off_queue = 0, off_redo = 0;
@@ -339,7 +369,7 @@ namespace fse {
 
 static int session_open(int32_t n, FsePlan *const *plans, void *const *images, const uint8_t *const *masks,
                         uint8_t *const *masks_out, const FseParamsC *p, int32_t dtype, const void *decay,
-                        int32_t decay_dim, int32_t *picks, int row_lo, int row_hi, cudaStream_t s,
+                        int32_t decay_dim, int32_t *picks, int row_lo, int row_hi, int groups, cudaStream_t s,
                         FseShard **out) {
     if (n < 1 || !plans || !images || !masks || !p || !decay || !out) return fail(FSE_EINVAL, "NULL argument");
     if (dtype != FSE_F64 && dtype != FSE_F32) return fail(FSE_EINVAL, "dtype");
@@ -376,26 +406,49 @@ static int session_open(int32_t n, FsePlan *const *plans, void *const *images, c
     for (int f = 0; f < n; ++f) n_levels = std::max(n_levels, (int)plans[f]->p.level_ptr.size() - 1);
     S->n_levels = n_levels;
     auto owned = [&](int b) { const int r = b / cols; return r >= row_lo && r < row_hi; };
-    // merged level lists: level L of every frame in one launch (owned rows only)
-    S->lvl_off.assign(n_levels + 1, 0);
-    S->edge.assign(n_levels, 0);
-    size_t n_entries = 0;
-    for (int l = 0; l < n_levels; ++l) {
-        S->lvl_off[l] = (int)n_entries;
+    // frame groups: contiguous frame ranges with about equal entry counts
+    groups = std::max(1, std::min(groups, n));
+    std::vector<int> gstart(groups + 1, n);
+    {
+        std::vector<long long> cnt(n, 0);
+        long long tot = 0;
         for (int f = 0; f < n; ++f) {
             const Plan &P = plans[f]->p;
-            if (l + 1 >= (int)P.level_ptr.size()) continue;
-            for (int i = P.level_ptr[l]; i < P.level_ptr[l + 1]; ++i) {
-                const int b = P.level_blocks[i];
-                if (!owned(b)) continue;
-                ++n_entries;
-                const int r = b / cols;
-                if (r < row_lo + R) S->edge[l] |= 1;
-                if (r >= row_hi - R) S->edge[l] |= 2;
+            for (int b : P.level_blocks) cnt[f] += owned(b) ? 1 : 0;
+            tot += cnt[f];
+        }
+        long long acc = 0;
+        int g = 0;
+        gstart[0] = 0;
+        for (int f = 0; f < n && g + 1 < groups; ++f) {
+            acc += cnt[f];
+            if (acc * groups >= tot * (g + 1) && f + 1 < n) gstart[++g] = f + 1;
+        }
+        groups = g + 1;
+        gstart[groups] = n;
+    }
+    S->groups = groups;
+    // level lists per group: level L of every frame of the group in one launch
+    S->lvl_off.assign((size_t)groups * n_levels + 1, 0);
+    S->edge.assign(n_levels, 0);
+    size_t n_entries = 0;
+    for (int g = 0; g < groups; ++g)
+        for (int l = 0; l < n_levels; ++l) {
+            S->lvl_off[(size_t)g * n_levels + l] = (int)n_entries;
+            for (int f = gstart[g]; f < gstart[g + 1]; ++f) {
+                const Plan &P = plans[f]->p;
+                if (l + 1 >= (int)P.level_ptr.size()) continue;
+                for (int i = P.level_ptr[l]; i < P.level_ptr[l + 1]; ++i) {
+                    const int b = P.level_blocks[i];
+                    if (!owned(b)) continue;
+                    ++n_entries;
+                    const int r = b / cols;
+                    if (r < row_lo + R) S->edge[l] |= 1;
+                    if (r >= row_hi - R) S->edge[l] |= 2;
+                }
             }
         }
-    }
-    S->lvl_off[n_levels] = (int)n_entries;
+    S->lvl_off[(size_t)groups * n_levels] = (int)n_entries;
     S->n_entries = n_entries;
     // one device staging buffer:
     //   uploaded: frame table | ranks | entries (level order)
@@ -405,7 +458,7 @@ static int session_open(int32_t n, FsePlan *const *plans, void *const *images, c
     const size_t off_rank = up256(sizeof(FrameDesc) * n);
     S->off_ent = off_rank + up256(sizeof(int32_t) * (size_t)nb * n);
     S->off_cnt = S->off_ent + up256(sizeof(int2) * std::max<size_t>(n_entries, 1));
-    S->off_next = S->off_cnt + up256(sizeof(int) * std::max(n_levels, 1));
+    S->off_next = S->off_cnt + up256(sizeof(int) * std::max(groups * n_levels, 1));
     S->off_done = S->off_next + 256;
     S->off_queue = S->off_done + up256(sizeof(int) * (size_t)nb * n);
     S->off_redo = S->off_queue + up256(sizeof(int) * std::max<size_t>(n_entries, 1));
@@ -429,13 +482,14 @@ static int session_open(int32_t n, FsePlan *const *plans, void *const *images, c
     }
     {
         size_t k = 0;
-        for (int l = 0; l < n_levels; ++l)
-            for (int f = 0; f < n; ++f) {
-                const Plan &P = plans[f]->p;
-                if (l + 1 >= (int)P.level_ptr.size()) continue;
-                for (int i = P.level_ptr[l]; i < P.level_ptr[l + 1]; ++i)
-                    if (owned(P.level_blocks[i])) ent[k++] = make_int2(f, P.level_blocks[i]);
-            }
+        for (int g = 0; g < groups; ++g)
+            for (int l = 0; l < n_levels; ++l)
+                for (int f = gstart[g]; f < gstart[g + 1]; ++f) {
+                    const Plan &P = plans[f]->p;
+                    if (l + 1 >= (int)P.level_ptr.size()) continue;
+                    for (int i = P.level_ptr[l]; i < P.level_ptr[l + 1]; ++i)
+                        if (owned(P.level_blocks[i])) ent[k++] = make_int2(f, P.level_blocks[i]);
+                }
     }
     // pageable source: staged by the driver before returning, so `host` may go
     ce = cudaMemcpyAsync(dev, host.data(), S->off_cnt, cudaMemcpyHostToDevice, s);
@@ -514,34 +568,66 @@ static int session_run(FseShard *S, int l0, int l1, bool whole, cudaStream_t s) 
         if (g_timing.on) ++g_timing.window_launches;
         l1 = l0;
     }
-    for (int l = l0; l < l1 && rc == FSE_OK; ++l) {
-        const int2 *lvl = reinterpret_cast<const int2 *>(dev + S->off_ent) + S->lvl_off[l];
-        const int cnt = S->lvl_off[l + 1] - S->lvl_off[l];
-        if (cnt == 0) continue;
-        if (S->fast) {
-            f.entries = lvl;
-            f.redo_list = redo + S->lvl_off[l];
-            f.redo_count = counters + l;
-            rc = fast_level(S->dtype, S->F1, S->guard, f, cnt, S->Mmax, S->Nmax, S->model_n, s);
-            if (rc == FSE_OK && S->guard) {
-                FastArgs r = f;
-                r.entries = redo + S->lvl_off[l];
-                r.count = counters + l;
-                rc = fast_redo(S->F1, r, cnt, S->Mmax, S->Nmax, S->model_n, s);
-            }
-        } else {
-            a.entries = lvl;
-            rc = S->dtype == FSE_F64
-                     ? dispatch<double, 0, false>(a, cnt, S->Mmax, S->Nmax, S->F1, S->F2, S->model_n, s)
-                     : dispatch<float, 0, false>(a, cnt, S->Mmax, S->Nmax, S->F1, S->F2, S->model_n, s);
+    // groups > 1: fork one stream per group off `s`, launch level-major
+    // (level l of every group before level l + 1), join back into `s`
+    const int G = S->groups;
+    std::vector<cudaStream_t> gs(G, s);
+    std::vector<cudaEvent_t> gev;
+    if (G > 1 && l1 > l0) {
+        gev.assign(G + 1, nullptr);
+        for (auto &e : gev)
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+                return fail(FSE_ECUDA, "event create");
+        cudaEventRecord(gev[G], s);
+        for (int g = 0; g < G; ++g) {
+            gs[g] = group_stream(g);
+            if (!gs[g]) return fail(FSE_ECUDA, "group stream");
+            cudaStreamWaitEvent(gs[g], gev[G], 0);
         }
-        if (g_timing.on) ++g_timing.window_launches;
+    }
+    for (int l = l0; l < l1 && rc == FSE_OK; ++l)
+        for (int g = 0; g < G && rc == FSE_OK; ++g) {
+            const size_t q = (size_t)g * S->n_levels + l;
+            const int2 *lvl = reinterpret_cast<const int2 *>(dev + S->off_ent) + S->lvl_off[q];
+            const int cnt = S->lvl_off[q + 1] - S->lvl_off[q];
+            if (cnt == 0) continue;
+            cudaStream_t sg = gs[g];
+            if (S->fast) {
+                f.entries = lvl;
+                f.redo_list = redo + S->lvl_off[q];
+                f.redo_count = counters + q;
+                rc = fast_level(S->dtype, S->F1, S->guard, f, cnt, S->Mmax, S->Nmax, S->model_n, sg);
+                if (rc == FSE_OK && S->guard) {
+                    FastArgs r = f;
+                    r.entries = redo + S->lvl_off[q];
+                    r.count = counters + q;
+                    rc = fast_redo(S->F1, r, cnt, S->Mmax, S->Nmax, S->model_n, sg);
+                }
+            } else {
+                a.entries = lvl;
+                rc = S->dtype == FSE_F64
+                         ? dispatch<double, 0, false>(a, cnt, S->Mmax, S->Nmax, S->F1, S->F2, S->model_n, sg)
+                         : dispatch<float, 0, false>(a, cnt, S->Mmax, S->Nmax, S->F1, S->F2, S->model_n, sg);
+            }
+            if (g_timing.on) ++g_timing.window_launches;
+        }
+    if (!gev.empty()) {
+        // join (also on failure, so `s` never runs ahead of queued group work)
+        for (int g = 0; g < G; ++g) {
+            cudaEventRecord(gev[g], gs[g]);
+            cudaStreamWaitEvent(s, gev[g], 0);
+        }
+        for (auto e : gev) cudaEventDestroy(e);
     }
     if (g_timing.on && S->guard && l1 > l0) {
+        // per (group, level) counters of levels [l0, l1)
+        const int nl = l1 - l0;
         int *hc = nullptr;
-        if (cudaMallocHost((void **)&hc, sizeof(int) * (l1 - l0)) == cudaSuccess) {
-            cudaMemcpyAsync(hc, counters + l0, sizeof(int) * (l1 - l0), cudaMemcpyDeviceToHost, s);
-            g_timing.redo.emplace_back(hc, l1 - l0);
+        if (cudaMallocHost((void **)&hc, sizeof(int) * G * nl) == cudaSuccess) {
+            for (int g = 0; g < G; ++g)
+                cudaMemcpyAsync(hc + g * nl, counters + (size_t)g * S->n_levels + l0, sizeof(int) * nl,
+                                cudaMemcpyDeviceToHost, s);
+            g_timing.redo.emplace_back(hc, G * nl);
         }
     }
     if (g_timing.on) {
@@ -582,8 +668,10 @@ int fse_conceal_frames(int32_t n, FsePlan *const *plans, void *const *images,
     if (!plans || !plans[0]) return fail(FSE_EINVAL, "NULL plan");
     cudaStream_t s = (cudaStream_t)stream;
     FseShard *S = nullptr;
+    // the dataflow executor walks one level-ordered list: one group
+    const int groups = fse::dataflow_enabled() ? 1 : fse::g_groups;
     int rc = fse::session_open(n, plans, images, masks, masks_out, p, dtype, decay, decay_dim, picks, 0,
-                               plans[0]->p.rows, s, &S);
+                               plans[0]->p.rows, groups, s, &S);
     if (rc) return rc;
     rc = fse::session_run(S, 0, S->n_levels, true, s);
     const int rc2 = fse::session_close(S, rc == FSE_OK, s);
@@ -598,7 +686,7 @@ int fse_shard_open(const FsePlan *plan, int32_t row_lo, int32_t row_hi, void *im
     void *im = image;
     uint8_t *mo = mask_out;
     return fse::session_open(1, &pl, &im, &mask, mask_out ? &mo : nullptr, p, dtype, decay, decay_dim,
-                             nullptr, row_lo, row_hi, (cudaStream_t)stream, out);
+                             nullptr, row_lo, row_hi, 1, (cudaStream_t)stream, out);
 }
 
 int fse_shard_levels(const FseShard *sh, int32_t *n_levels, int32_t *edge_flags) {

@@ -267,9 +267,32 @@ def test_dataflow_equals_level_launches(cfg, B, F, order, prec):
         L.fse_set_dataflow(0)
         b, bm, _ = P.conceal(img, mask, p, order, precision=prec)
     finally:
-        L.fse_set_dataflow(1)
+        L.fse_set_dataflow(0)
     assert a.tobytes() == b.tobytes()
     np.testing.assert_array_equal(am, bm)
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_frame_groups_equal_one_launch_sequence(prec):
+    """Frame groups on forked streams (fse_set_groups) compute the same images
+    and masks as one level-launch sequence over all frames."""
+    from paper_2207_00233_b200 import _lib
+
+    sc = [synth.config_scene(4, f) for f in range(3)]
+    imgs = np.stack([s[0][:160, :224] for s in sc])
+    msks = np.stack([s[1][:160, :224] for s in sc])
+    p = P.FseParams(d=14, iterations=30, block_size=4, fft_size=64)
+    L = _lib.lib()
+    outs = []
+    try:
+        for g in (1, 2, 3):
+            assert L.fse_set_groups(g) == 0
+            o, m, _ = P.conceal_batch(imgs, msks, p, precision=prec, reports=False)
+            outs.append((o.tobytes(), m.tobytes()))
+    finally:
+        L.fse_set_groups(2)
+    assert outs[0] == outs[1] == outs[2]
+    assert L.fse_set_groups(0) != 0 and L.fse_set_groups(9) != 0
 
 
 @pytest.mark.parametrize("B,F", [(2, 32), (4, 64), (8, 128)])
