@@ -199,6 +199,18 @@ __device__ __forceinline__ unsigned long long energy_key(double e) {
     return (unsigned long long)__double_as_longlong(e);
 }
 
+// |g|^2 with one pinned rounding sequence (y*y, then fma(x, x, .)), so the
+// value found again by the winner search equals the one maximised
+__device__ __forceinline__ float energy(float2 g) { return __fmaf_rn(g.x, g.x, __fmul_rn(g.y, g.y)); }
+__device__ __forceinline__ double energy(double2 g) { return __fma_rn(g.x, g.x, __dmul_rn(g.y, g.y)); }
+
+__device__ __forceinline__ unsigned warp_max_k(unsigned k) { return warp_max_u32(k); }
+__device__ __forceinline__ unsigned long long warp_max_k(unsigned long long k) {
+    const unsigned mh = warp_max_u32((unsigned)(k >> 32));
+    const unsigned ml = warp_max_u32((unsigned)(k >> 32) == mh ? (unsigned)k : 0u);
+    return ((unsigned long long)mh << 32) | ml;
+}
+
 // Warp argmax of (key, lin): largest key, ties to the smallest lin (the
 // reference's first maximum in row-major order, _kernel.pyx:32-44).  Returns
 // the winning key and lin, uniform across the warp.
@@ -626,8 +638,16 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     unsigned blin = 0xFFFFFFFFu;       // row-major index of the best bin, none yet
     const unsigned lin0 = (unsigned)(u0 * F + v);
     T2 bg = T2{0, 0};  // g of the best bin, carried along (no register indexing later)
+    // LAZY: only the running maximum energy is kept per bin (one FMNMX); the
+    // few lanes holding the CTA maximum find its bin again after the reduction
+    // (a second barrier), instead of every bin carrying index and g along.
+    constexpr bool LAZY = IS_F32 && CL == 1 && !GUARD;
+    T tmax = (T)0;
+    using KeyT = decltype(energy_key((T)0));
     auto track = [&](int j, T e) {
-        if constexpr (IS_F32 && GUARD) {
+        if constexpr (LAZY) {
+            tmax = fmax(tmax, e);  // NaN never wins, like the strict '>' scan
+        } else if constexpr (IS_F32 && GUARD) {
             const unsigned key = (__float_as_uint((float)e) & ~0x1Fu) | (unsigned)(31 - j);
             if (key > k1) bg = G[j];
             k2 = max(k2, min(k1, key));
@@ -643,7 +663,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
 
 #pragma unroll
     for (int j = 0; j < NB; ++j)
-        if ((valid >> j) & 1u) track(j, G[j].x * G[j].x + G[j].y * G[j].y);
+        if ((valid >> j) & 1u) track(j, energy(G[j]));
 
     // fp32: gamma / sum(w) folded into one factor (gamma = 0.5 keeps the
     // products bit-identical); MODE 1 logs p itself
@@ -653,7 +673,15 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         // ---- (1) CTA-wide argmax (+ runner-up for the guard), one barrier
         FastSlot<T> *sl = slots + (it & 1) * NWT;
         ArgSlot<T> *asl = asl0 + (it & 1) * NWT;
-        if constexpr (IS_F32 && GUARD) {
+        // LAZY slots: per-warp maximum keys (double-buffered), then the
+        // candidate warps' (lin, g); the key region is 2 NWT x 8 bytes
+        KeyT *ska = reinterpret_cast<KeyT *>(reinterpret_cast<unsigned long long *>(slots) + (it & 1) * NWT);
+        ArgSlot<T> *skb = reinterpret_cast<ArgSlot<T> *>(reinterpret_cast<unsigned long long *>(slots) + 2 * NWT);
+        KeyT wk = 0;
+        if constexpr (LAZY) {
+            wk = warp_max_k(energy_key(tmax));
+            if (lane == 0) ska[warp] = wk;
+        } else if constexpr (IS_F32 && GUARD) {
             const unsigned w1 = warp_max_u32(k1);
             const int wl = __ffs(__ballot_sync(0xffffffffu, k1 == w1)) - 1;
             const unsigned w2 = warp_max_u32(lane == wl ? k2 : k1);
@@ -691,7 +719,52 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         else __syncthreads();
         int a, b;
         T2 gwin;
-        if constexpr (IS_F32 && GUARD) {
+        if constexpr (LAZY) {
+            const bool in = lane < NWT;
+            const KeyT uk = in ? ska[lane] : (KeyT)0;
+            const KeyT gk = warp_max_k(uk);
+            if (gk == 0) {
+                // no bin above 0 (all energies 0 or NaN): the reference's
+                // strict-'>' scan from -1 keeps (0, 0) (_kernel.pyx:32-44), g = 0
+                a = b = 0;
+                gwin = T2{0, 0};
+            } else {
+                if (wk == gk) {
+                    // a candidate warp: its lanes at the maximum find their first
+                    // (row-major) bin at that energy; the smallest lin is the warp's
+                    unsigned mylin = 0xFFFFFFFFu;
+                    T2 myg = T2{0, 0};
+                    if (energy_key(tmax) == gk) {
+#pragma unroll
+                        for (int j = NB - 1; j >= 0; --j) {
+                            const bool inr = (j < NB - 1) || (C::NSEGS % NWT == 0) || (u0 + RSTEP * j < R1);
+                            const bool ok = (j == 0 || j == NB - 1) ? ((valid >> j) & 1u) != 0 : inr;
+                            if (ok && energy_key(energy(G[j])) == gk) {
+                                mylin = lin0 + (unsigned)(j * RSTEP * F);
+                                myg = G[j];
+                            }
+                        }
+                    }
+                    const unsigned wl = warp_min_u32(mylin);
+                    if (mylin == wl) {
+                        ArgSlot<T> mine;
+                        mine.key = gk;
+                        mine.lin = wl;
+                        mine.gre = myg.x;
+                        mine.gim = myg.y;
+                        skb[warp] = mine;
+                    }
+                }
+                __syncthreads();
+                const bool cand = in && uk == gk;
+                const unsigned ul = cand ? skb[lane].lin : 0xFFFFFFFFu;
+                const unsigned glin = warp_min_u32(ul);
+                const int gw = __ffs(__ballot_sync(0xffffffffu, cand && ul == glin)) - 1;
+                a = (int)(glin / F);
+                b = (int)(glin & (F - 1));
+                gwin = T2{skb[gw].gre, skb[gw].gim};
+            }
+        } else if constexpr (IS_F32 && GUARD) {
             const unsigned long long uk = lane < NW ? sl[lane].key : 0ull;
             const unsigned long long gk = warp_max_key(uk);
             const int gw = __ffs(__ballot_sync(0xffffffffu, uk == gk)) - 1;
@@ -781,6 +854,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         k2 = 0;
         best = (T)0;
         blin = 0xFFFFFFFFu;
+        tmax = (T)0;
         const T2 mS = T2{-gpr, -gpr}, qv = T2{gpi, -gpi};
         // loads of a group of LG bins are issued before its math (smem latency)
         constexpr int LG = IS_F32 ? 4 : 2;
@@ -808,7 +882,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
                 if (inr) {
                     if constexpr (IS_F32) G[j] = spectral_update_bc(G[j], wl[q], wh[q], -gpr, gpi);
                     else G[j] = spectral_update(G[j], wl[q], wh[q], mS, qv);
-                    const T e = G[j].x * G[j].x + G[j].y * G[j].y;
+                    const T e = energy(G[j]);
                     if (j == 0 || j == NB - 1) {
                         if ((valid >> j) & 1u) track(j, e);
                     } else {

@@ -63,7 +63,10 @@ int fast_supported(int dtype, int F, int Mmax, int Nmax, int model_n) {
 
 template <class C, int MODE, bool GUARD>
 static int launch(const FastArgs &a, int grid, int Mmax, int Nmax, int model_n, cudaStream_t s) {
-    const FastLayout L = fast_layout<typename C::T>(C::F, C::NWT, Mmax, Nmax, model_n, a.iterations, C::EXT);
+    FastLayout L = fast_layout<typename C::T>(C::F, C::NWT, Mmax, Nmax, model_n, a.iterations, C::EXT);
+#ifdef FSE_SMEM_PAD
+    L.total += FSE_SMEM_PAD;  // dev: occupancy sensitivity experiments
+#endif
     auto kern = fse_fast_kernel<C, MODE, GUARD>;
     static thread_local size_t configured = 0;  // largest dynamic smem size set so far
     if (L.total > configured) {
