@@ -51,6 +51,61 @@ static int g_groups = [] {
     return std::max(1, std::min(v, 8));
 }();
 
+// Pinned host staging buffers for the session uploads (frame table, ranks,
+// level entry lists; tens of MB for a 64-frame batch).  A pageable source
+// would make cudaMemcpyAsync wait for the stream's earlier kernels and leave
+// the GPU idle while the driver stages it; from pinned memory the copy is
+// queued and the host returns at once.  A buffer is reused once the copy
+// that last read it has completed (its event).
+struct PinnedStage {
+    void *p = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev = nullptr;
+    bool busy = false;  // acquired, its copy not queued yet
+};
+static std::mutex g_stage_mu;
+static std::vector<PinnedStage> g_stage;
+
+static int stage_acquire(size_t bytes, int *slot, unsigned char **ptr) {
+    std::lock_guard<std::mutex> lk(g_stage_mu);
+    int pick = -1;
+    for (int i = 0; i < (int)g_stage.size(); ++i) {
+        PinnedStage &b = g_stage[i];
+        if (b.busy || (b.ev && cudaEventQuery(b.ev) != cudaSuccess)) continue;  // in use / copy in flight
+        if (b.cap >= bytes) {
+            pick = i;
+            break;
+        }
+        if (pick < 0) pick = i;  // free but small: grow this one
+    }
+    if (pick < 0) {
+        g_stage.emplace_back();
+        pick = (int)g_stage.size() - 1;
+    }
+    PinnedStage &b = g_stage[pick];
+    if (b.cap < bytes) {
+        if (b.p) cudaFreeHost(b.p);
+        b.p = nullptr;
+        b.cap = 0;
+        const size_t cap = std::max(bytes, (size_t)1 << 20) * 5 / 4;
+        if (cudaMallocHost(&b.p, cap) != cudaSuccess) return fail(FSE_ENOMEM, "pinned staging alloc");
+        b.cap = cap;
+    }
+    if (!b.ev && cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming) != cudaSuccess)
+        return fail(FSE_ECUDA, "event create");
+    b.busy = true;
+    *slot = pick;
+    *ptr = static_cast<unsigned char *>(b.p);
+    return FSE_OK;
+}
+
+// the copy that reads slot's buffer has been queued on s
+static void stage_release(int slot, cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(g_stage_mu);
+    cudaEventRecord(g_stage[slot].ev, s);
+    g_stage[slot].busy = false;
+}
+
 // Per-device pool of non-blocking streams for the groups (created once).
 static cudaStream_t group_stream(int g) {
     constexpr int MAXD = 16, MAXG = 8;
@@ -463,16 +518,22 @@ static int session_open(int32_t n, FsePlan *const *plans, void *const *images, c
     S->off_queue = S->off_done + up256(sizeof(int) * (size_t)nb * n);
     S->off_redo = S->off_queue + up256(sizeof(int) * std::max<size_t>(n_entries, 1));
     const size_t bytes = S->off_redo + sizeof(int2) * std::max<size_t>(n_entries, 1);
-    std::vector<unsigned char> host(S->off_cnt);
+    int slot = -1;
+    unsigned char *host = nullptr;
+    if (int rc = stage_acquire(S->off_cnt, &slot, &host)) {
+        delete S;
+        return rc;
+    }
     cudaError_t ce = cudaMallocAsync((void **)&S->dev, bytes, s);
     if (ce != cudaSuccess) {
+        stage_release(slot, s);
         delete S;
         return fail(FSE_ECUDA, std::string("staging alloc: ") + cudaGetErrorString(ce));
     }
     unsigned char *dev = S->dev;
-    FrameDesc *fdh = reinterpret_cast<FrameDesc *>(host.data());
-    int32_t *rk = reinterpret_cast<int32_t *>(host.data() + off_rank);
-    int2 *ent = reinterpret_cast<int2 *>(host.data() + S->off_ent);
+    FrameDesc *fdh = reinterpret_cast<FrameDesc *>(host);
+    int32_t *rk = reinterpret_cast<int32_t *>(host + off_rank);
+    int2 *ent = reinterpret_cast<int2 *>(host + S->off_ent);
     for (int f = 0; f < n; ++f) {
         fdh[f].image = images[f];
         fdh[f].mask = masks[f];
@@ -491,8 +552,9 @@ static int session_open(int32_t n, FsePlan *const *plans, void *const *images, c
                         if (owned(P.level_blocks[i])) ent[k++] = make_int2(f, P.level_blocks[i]);
                 }
     }
-    // pageable source: staged by the driver before returning, so `host` may go
-    ce = cudaMemcpyAsync(dev, host.data(), S->off_cnt, cudaMemcpyHostToDevice, s);
+    // pinned source: queued; the buffer is reusable once this copy completes
+    ce = cudaMemcpyAsync(dev, host, S->off_cnt, cudaMemcpyHostToDevice, s);
+    stage_release(slot, s);
     if (ce == cudaSuccess) ce = cudaMemsetAsync(dev + S->off_cnt, 0, S->off_queue - S->off_cnt, s);
     if (ce == cudaSuccess) ce = cudaMemsetAsync(dev + S->off_queue, 0xFF, S->off_redo - S->off_queue, s);
     if (ce != cudaSuccess) {
