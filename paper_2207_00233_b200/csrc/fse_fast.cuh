@@ -597,21 +597,6 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     }
     __syncthreads();
 
-    // model samples of the block owned by this thread (q = t, t + NT)
-    T mval[2] = {(T)0, (T)0};
-    int mi[2] = {0, 0}, mj[2] = {0, 0};
-    bool mown[2] = {false, false};
-    if constexpr (MODE == 0) {
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const int q = lane * NW + warp + k * NT;  // spread over the warps
-            mown[k] = q < bh * bw && crank == 0;     // the cluster's CTA 0 writes the block
-            if (mown[k]) {
-                mi[k] = br0 + q / bw;
-                mj[k] = bc0 + q % bw;
-            }
-        }
-    }
     const T gamma = (T)A.gamma;
     const T tot = (T)total;
     const T inv_tot = (T)1 / tot;
@@ -894,7 +879,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     }
 
     // ---- model over the block: sum_it 2 Re(gamma p_it e^{+j 2 pi (a i + b j)/F}),
-    // fse.py:159 restricted to the block rect, accumulated in iteration order
+    // fse.py:159 restricted to the block rect
     if constexpr (MODE == 0) {
         __syncthreads();
         if (picks_out && crank == 0)
@@ -902,25 +887,42 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
                 picks_out[2 * i] = hist[i].a;
                 picks_out[2 * i + 1] = hist[i].b;
             }
-#pragma unroll
-        for (int k = 0; k < 2; ++k)
-            if (mown[k])
-                for (int it = 0; it < I; ++it) {
-                    const PickRec<T> h = hist[it];
-                    const T2 ph = tw[(h.a * mi[k] + h.b * mj[k]) & (F - 1)];
-                    mval[k] += (T)2 * (h.gpr * ph.x - h.gpi * ph.y);
-                }
-    }
-
-    // ---- write-back of the block's LOST samples (conceal.py:61-66)
-    if constexpr (MODE == 0) {
+        // every thread sums the iterations it = r (mod nsub) of one sample q
+        // (nsub = NT / samples subsets), then one thread per sample adds the
+        // nsub partials in subset order; the W plane is dead, so the partials
+        // reuse its bytes.  More samples than threads: all iterations per sample.
+        const int nsamp = bh * bw;
         IT *img = reinterpret_cast<IT *>(fd->image);
-#pragma unroll
-        for (int k = 0; k < 2; ++k)
-            if (mown[k]) {
-                const size_t off = (size_t)(wr0 + mi[k]) * A.W + (wc0 + mj[k]);
-                if (fd->mask[off] == FSE_LOST) img[off] = (IT)mval[k];
+        auto model = [&](int q, int r0, int step) -> T {
+            const int mi = br0 + q / bw, mj = bc0 + q % bw;
+            T acc = (T)0;
+            for (int it = r0; it < I; it += step) {
+                const PickRec<T> h = hist[it];
+                const T2 ph = tw[(h.a * mi + h.b * mj) & (F - 1)];
+                acc += (T)2 * (h.gpr * ph.x - h.gpi * ph.y);
             }
+            return acc;
+        };
+        // write-back of the block's LOST samples (conceal.py:61-66)
+        auto store = [&](int q, T val) {
+            const size_t off = (size_t)(wr0 + br0 + q / bw) * A.W + (wc0 + bc0 + q % bw);
+            if (fd->mask[off] == FSE_LOST) img[off] = (IT)val;
+        };
+        if (crank == 0) {  // the cluster's CTA 0 writes the block
+            if (nsamp <= NT) {
+                const int nsub = NT / nsamp, q = t % nsamp, r = t / nsamp;
+                T *red2 = reinterpret_cast<T *>(big);
+                if (r < nsub) red2[r * nsamp + q] = model(q, r, nsub);
+                __syncthreads();
+                if (t < nsamp) {
+                    T v = (T)0;
+                    for (int k = 0; k < nsub; ++k) v += red2[k * nsamp + t];
+                    store(t, v);
+                }
+            } else {
+                for (int q = t; q < nsamp; q += NT) store(q, model(q, 0, 1));
+            }
+        }
     }
     // keep this CTA's shared memory alive until the cluster is done with it
     if constexpr (CL > 1) cooperative_groups::this_cluster().sync();
