@@ -548,10 +548,19 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     __syncthreads();
     partials(Yw);
     __syncthreads();
+    // W half rows 0..F/2; with EXT (one CTA per window) also the negative
+    // rows W[-u][-v] = conj W[u][v] at once: they land in the dead x/w/Y
+    // staging bytes below the half rows, while `part` (above them) is still
+    // being read by other threads
+    constexpr bool MIRROR_NOW = C::EXT && CL == 1;
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
         const int u = u0 + RSTEP * j;
-        if (u < R1) Wext[(u + (C::EXT ? F / 2 : 0)) * F + v] = combine(u);
+        if (u < R1) {
+            const T2 wv = combine(u);
+            Wext[(u + (C::EXT ? F / 2 : 0)) * F + v] = wv;
+            if (MIRROR_NOW && u >= 1) Wext[(F / 2 - u) * F + ((F - v) & (F - 1))] = T2{wv.x, -wv.y};
+        }
     }
     if constexpr (CL > 1) {
         // every CTA of the cluster holds the whole W: fetch the half rows the
@@ -577,7 +586,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         }
     }
     // extension rows: W[-s] = conj W[s] reflected, W[F] = W[0]
-    for (int idx = t; C::EXT && idx < (F / 2) * F; idx += NT) {
+    for (int idx = t; C::EXT && !MIRROR_NOW && idx < (F / 2) * F; idx += NT) {
         const int rr = idx / F, c = idx - rr * F;  // ext row rr in [0, F/2): W row rr - F/2
         const int s = F / 2 - rr;                  // W row -s, s in [1, F/2]
         const T2 src = Wext[(s + F / 2) * F + ((F - c) & (F - 1))];
