@@ -522,13 +522,12 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         T2 acc = pr[0];
 #pragma unroll
         for (int r = 1; r < 4; ++r) {
+            // + pv (-j)^k, k = q r mod 4, branch-free (q differs within a warp):
+            // k=0 (x, y), 1 (y, -x), 2 (-x, -y), 3 (-y, x)
             const T2 pv = pr[r * QW];
-            switch ((q4 * r) & 3) {  // (-j)^{q r}
-                case 0: acc = cadd(acc, pv); break;
-                case 1: acc = cadd(acc, T2{pv.y, -pv.x}); break;
-                case 2: acc = csub(acc, pv); break;
-                default: acc = cadd(acc, T2{-pv.y, pv.x}); break;
-            }
+            const int k = (q4 * r) & 3;
+            const T x = (k & 1) ? pv.y : pv.x, y = (k & 1) ? pv.x : pv.y;
+            acc = cadd(acc, T2{(k & 2) ? -x : x, (k == 1 || k == 2) ? -y : y});
         }
         return acc;
     };
