@@ -282,6 +282,15 @@ __device__ __forceinline__ float2 spectral_update_bc(float2 g, float2 lo, float2
     return cfma(float2{D.y, -D.x}, float2{gpi, gpi}, g);
 }
 
+// a / b from the correctly rounded reciprocal rb = 1/b: q = a rb, then one
+// FMA residual correction, q + (a - q b) rb, which is the correctly rounded
+// quotient for normal operands (Markstein) -- the result of a / b, at 3
+// DFMA-pipe operations instead of a full division per use
+__device__ __forceinline__ double div_by(double a, double b, double rb) {
+    const double q = a * rb;
+    return fma(fma(-q, b, a), rb, q);
+}
+
 // acc += z * e^{-j theta}, tw = (cos theta, sin theta): the forward-DFT MAC
 template <typename T2>
 __device__ __forceinline__ T2 dft_mac(T2 acc, T2 z, T2 tw) {
@@ -805,8 +814,8 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
             gpr = gwin.x * ginv;
             gpi = gwin.y * ginv;
         } else {
-            gpr = gamma * (gwin.x / tot);
-            gpi = gamma * (gwin.y / tot);
+            gpr = gamma * div_by(gwin.x, tot, inv_tot);
+            gpi = gamma * div_by(gwin.y, tot, inv_tot);
         }
         if constexpr (MODE == 1) {
             if (gwarp == 0 && lane == 0) {
@@ -816,8 +825,8 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
                     plog[2 * it] = gwin.x * inv_tot;
                     plog[2 * it + 1] = gwin.y * inv_tot;
                 } else {
-                    plog[2 * it] = gwin.x / tot;
-                    plog[2 * it + 1] = gwin.y / tot;
+                    plog[2 * it] = div_by(gwin.x, tot, inv_tot);
+                    plog[2 * it + 1] = div_by(gwin.y, tot, inv_tot);
                 }
             }
         }
