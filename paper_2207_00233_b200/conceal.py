@@ -21,6 +21,7 @@ levels merged into one launch each (frame-parallel, BASELINE config 4).
 from __future__ import annotations
 
 import ctypes
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -238,6 +239,64 @@ def conceal(image, mask, params: FseParams | None = None, order: str = OPTIMIZED
     return out_img, out_msk, rep
 
 
+_COPY_STREAMS: dict = {}
+
+
+def _copy_stream():
+    """One side stream per device for conceal_batch's overlapped copies."""
+    import torch
+
+    dev = torch.cuda.current_device()
+    s = _COPY_STREAMS.get(dev)
+    if s is None:
+        s = _COPY_STREAMS[dev] = torch.cuda.Stream(device=dev)
+    return s
+
+
+def _chunk_bounds(n: int) -> list:
+    """Frame chunk boundaries of conceal_batch's staged pipeline: a small first
+    chunk (planned while nothing else can run; the rest is planned while it
+    computes) and the remainder.  Finer schedules (e.g. 1/16, 2/16, 11/16, 2/16,
+    which expose less of the final download) measured equal on config 4: the
+    narrower level launches cost what the overlap gains.  FSE_CHUNKS="a,b,..."
+    (fractions of n) overrides, for experiments."""
+    env = os.environ.get("FSE_CHUNKS")
+    if env:
+        fr = [float(x) for x in env.split(",")]
+    elif n >= 4:
+        fr = [1 / 8, 7 / 8]
+    else:
+        fr = [1.0]
+    bounds, acc = [0], 0.0
+    for f in fr:
+        acc += f
+        b = min(n, max(bounds[-1] + 1, int(round(acc * n))))
+        if b > bounds[-1]:
+            bounds.append(b)
+    if bounds[-1] < n:
+        bounds.append(n)
+    return bounds
+
+
+_BATCH_BUFS: dict = {}
+_TRACE = bool(os.environ.get("FSE_E2E_TRACE"))
+
+
+def _batch_buffers(n, H, W, in_dtype, tdt):
+    """(input-dtype image, working image, mask, mask-out) device buffers of one
+    batch shape, kept for the next call (the last shape only)."""
+    import torch
+
+    key = (torch.cuda.current_device(), n, H, W, in_dtype, tdt)
+    if key not in _BATCH_BUFS:
+        _BATCH_BUFS.clear()
+        img_d = torch.empty((n, H, W), dtype=tdt, device="cuda")
+        img_in = img_d if in_dtype == tdt else torch.empty((n, H, W), dtype=in_dtype, device="cuda")
+        msk_d = torch.empty((n, H, W), dtype=torch.uint8, device="cuda")
+        _BATCH_BUFS[key] = (img_in, img_d, msk_d, torch.empty_like(msk_d))
+    return _BATCH_BUFS[key]
+
+
 def conceal_batch(images, masks, params: FseParams | None = None, order: str = OPTIMIZED,
                   precision: str = "fp32", plan_threads: int = 0, reports: bool = True,
                   out_images=None, out_masks=None):
@@ -271,23 +330,80 @@ def conceal_batch(images, masks, params: FseParams | None = None, order: str = O
         raise ValueError("images and masks must both be [n, H, W]")
     t0 = time.perf_counter()
     tdt = torch.float64 if precision == "fp64" else torch.float32
-    # uploads are queued first (async from pinned memory); planning overlaps them
-    # and the device work of the first frames (plan_and_run)
-    img_d = imgs.to(device="cuda", non_blocking=True).to(tdt)
-    msk_d = msks.to(device="cuda", non_blocking=True)
-    out_d = torch.empty_like(msk_d)
-    plans = plan_and_run(list(msks.numpy()), list(img_d), list(msk_d), list(out_d), params,
-                         precision, order, plan_threads)
-    out_img = out_images if out_images is not None else torch.empty(img_d.shape, dtype=tdt, pin_memory=True)
-    out_msk = out_masks if out_masks is not None else torch.empty(out_d.shape, dtype=torch.uint8,
+    n, H, W = imgs.shape
+    out_img = out_images if out_images is not None else torch.empty((n, H, W), dtype=tdt, pin_memory=True)
+    out_msk = out_masks if out_masks is not None else torch.empty((n, H, W), dtype=torch.uint8,
                                                                    pin_memory=True)
-    if tuple(out_img.shape) != tuple(img_d.shape) or out_img.dtype != tdt:
+    if tuple(out_img.shape) != (n, H, W) or out_img.dtype != tdt:
         raise ValueError("out_images has the wrong shape or dtype")
-    if tuple(out_msk.shape) != tuple(out_d.shape) or out_msk.dtype != torch.uint8:
+    if tuple(out_msk.shape) != (n, H, W) or out_msk.dtype != torch.uint8:
         raise ValueError("out_masks has the wrong shape or dtype")
-    out_img.copy_(img_d, non_blocking=True)
-    out_msk.copy_(out_d, non_blocking=True)
-    torch.cuda.current_stream().synchronize()
+    # Staged pipeline (frames are independent):
+    #   main stream: upload chunk 1 -> its levels -> [rest uploaded] -> rest's levels -> download rest
+    #   copy stream: upload rest (during chunk 1's levels) -> download chunk 1 (during the rest's)
+    # The first chunk (~1/8) is planned while its upload runs, the rest while chunk 1 computes.
+    main = torch.cuda.current_stream()
+    copy = _copy_stream()
+    # device buffers persist across calls of one shape (no allocator traffic,
+    # which would serialise the two streams); every call ends synchronised
+    img_in, img_d, msk_d, out_d = _batch_buffers(n, H, W, imgs.dtype, tdt)
+    mh = msks.numpy()
+    bounds = _chunk_bounds(n)
+
+    def upload(lo, hi):
+        if img_in is img_d:
+            img_d[lo:hi].copy_(imgs[lo:hi], non_blocking=True)
+        else:
+            img_in[lo:hi].copy_(imgs[lo:hi], non_blocking=True)
+            img_d[lo:hi].copy_(img_in[lo:hi])
+        msk_d[lo:hi].copy_(msks[lo:hi], non_blocking=True)
+
+    def download(lo, hi):
+        out_img[lo:hi].copy_(img_d[lo:hi], non_blocking=True)
+        out_msk[lo:hi].copy_(out_d[lo:hi], non_blocking=True)
+
+    trace = [("start", time.perf_counter())] if _TRACE else None
+
+    def mark(what):
+        if trace is not None:
+            trace.append((what, time.perf_counter()))
+
+    # chunk 0 is uploaded on the main stream; the rest on the copy stream while
+    # chunk 0 computes.  Each chunk is planned while the previous one computes;
+    # every chunk but the last is downloaded on the copy stream while the next
+    # one computes.
+    lo0, hi0 = bounds[0], bounds[1]
+    upload(lo0, hi0)
+    up = None
+    if len(bounds) > 2:
+        with torch.cuda.stream(copy):
+            upload(hi0, n)
+            up = copy.record_event()
+    mark("upload")
+    plans = []
+    for c in range(len(bounds) - 1):
+        lo, hi = bounds[c], bounds[c + 1]
+        pl = build_plans(list(mh[lo:hi]), params, order, plan_threads)
+        mark(f"plan{c}")
+        if c == 1:
+            main.wait_event(up)
+        run_frames_device(pl, list(img_d[lo:hi]), list(msk_d[lo:hi]), list(out_d[lo:hi]), params, precision)
+        mark(f"run{c}")
+        plans += pl
+        if hi < n:
+            done = main.record_event()
+            with torch.cuda.stream(copy):
+                copy.wait_event(done)
+                download(lo, hi)
+        else:
+            download(lo, hi)
+    main.wait_stream(copy)
+    mark("download")
+    main.synchronize()
+    mark("sync")
+    if trace is not None:
+        print("conceal_batch: " + "  ".join(f"{w} {1e3 * (t - trace[i][1]):.1f}"
+                                            for i, (w, t) in enumerate(trace[1:])), flush=True)
     wall = time.perf_counter() - t0
     reps = [_report(p, order, 1, wall) for p in plans] if reports else None
     return out_img.numpy(), out_msk.numpy(), reps

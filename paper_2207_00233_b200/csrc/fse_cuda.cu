@@ -67,32 +67,35 @@ static std::mutex g_stage_mu;
 static std::vector<PinnedStage> g_stage;
 
 static int stage_acquire(size_t bytes, int *slot, unsigned char **ptr) {
+    // the smallest idle buffer that fits; otherwise a new one.  Buffers are
+    // never freed here: cudaFreeHost would synchronise the device and drain
+    // the level pipeline.  Past 16 buffers, wait for the oldest fitting one.
     std::lock_guard<std::mutex> lk(g_stage_mu);
+    auto idle = [](const PinnedStage &b) { return !b.busy && (!b.ev || cudaEventQuery(b.ev) == cudaSuccess); };
     int pick = -1;
-    for (int i = 0; i < (int)g_stage.size(); ++i) {
-        PinnedStage &b = g_stage[i];
-        if (b.busy || (b.ev && cudaEventQuery(b.ev) != cudaSuccess)) continue;  // in use / copy in flight
-        if (b.cap >= bytes) {
+    for (int i = 0; i < (int)g_stage.size(); ++i)
+        if (g_stage[i].cap >= bytes && idle(g_stage[i]) && (pick < 0 || g_stage[i].cap < g_stage[pick].cap))
             pick = i;
-            break;
-        }
-        if (pick < 0) pick = i;  // free but small: grow this one
+    if (pick < 0 && g_stage.size() >= 16) {
+        for (int i = 0; i < (int)g_stage.size(); ++i)
+            if (g_stage[i].cap >= bytes && !g_stage[i].busy) {
+                cudaEventSynchronize(g_stage[i].ev);
+                pick = i;
+                break;
+            }
     }
     if (pick < 0) {
-        g_stage.emplace_back();
+        PinnedStage b;
+        b.cap = std::max(bytes, (size_t)1 << 20) * 5 / 4;
+        if (cudaMallocHost(&b.p, b.cap) != cudaSuccess) return fail(FSE_ENOMEM, "pinned staging alloc");
+        if (cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming) != cudaSuccess) {
+            cudaFreeHost(b.p);
+            return fail(FSE_ECUDA, "event create");
+        }
+        g_stage.push_back(b);
         pick = (int)g_stage.size() - 1;
     }
     PinnedStage &b = g_stage[pick];
-    if (b.cap < bytes) {
-        if (b.p) cudaFreeHost(b.p);
-        b.p = nullptr;
-        b.cap = 0;
-        const size_t cap = std::max(bytes, (size_t)1 << 20) * 5 / 4;
-        if (cudaMallocHost(&b.p, cap) != cudaSuccess) return fail(FSE_ENOMEM, "pinned staging alloc");
-        b.cap = cap;
-    }
-    if (!b.ev && cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming) != cudaSuccess)
-        return fail(FSE_ECUDA, "event create");
     b.busy = true;
     *slot = pick;
     *ptr = static_cast<unsigned char *>(b.p);

@@ -194,13 +194,27 @@ def test_all_lost_and_retry_sweeps():
     assert len(seen) == len(set(seen)) == 64
 
 
-def test_conceal_batch_equals_per_frame():
-    frames = [synth.synthetic_frame(96, 160, 50 + f, 6, 3) for f in range(3)]
-    masks = [synth.loss_mask(96, 160, "mixed", 0.25, 60 + f) for f in range(3)]
+@pytest.mark.parametrize("nf", [3, 9])
+def test_conceal_batch_equals_per_frame(nf):
+    """One-chunk batches (< 4 frames) and the staged pipeline (first chunk, the
+    rest uploaded and downloaded on the copy stream) equal per-frame conceal."""
+    import torch
+
+    frames = [synth.synthetic_frame(96, 160, 50 + f, 6, 3) for f in range(nf)]
+    masks = [synth.loss_mask(96, 160, "mixed", 0.25, 60 + f) for f in range(nf)]
     p = P.FseParams(d=14, iterations=40, block_size=4, fft_size=64)
     for prec in ("fp64", "fp32"):
-        imgs, msks, reps = P.conceal_batch(np.stack(frames), np.stack(masks), p, precision=prec)
-        for f in range(3):
+        if nf > 3:  # pinned uint8 inputs and reused pinned outputs, as bench.py's e2e
+            ih = torch.from_numpy(np.stack(frames).astype(np.uint8)).pin_memory()
+            frames = [f.astype(np.uint8) for f in frames]
+            mh = torch.from_numpy(np.stack(masks)).pin_memory()
+            tdt = torch.float64 if prec == "fp64" else torch.float32
+            oi = torch.empty(ih.shape, dtype=tdt, pin_memory=True)
+            om_ = torch.empty(mh.shape, dtype=torch.uint8, pin_memory=True)
+            imgs, msks, reps = P.conceal_batch(ih, mh, p, precision=prec, out_images=oi, out_masks=om_)
+        else:
+            imgs, msks, reps = P.conceal_batch(np.stack(frames), np.stack(masks), p, precision=prec)
+        for f in range(nf):
             one, om, rep = P.conceal(frames[f], masks[f], p, precision=prec)
             assert imgs[f].astype(np.float64).tobytes() == one.tobytes()
             np.testing.assert_array_equal(msks[f], om)

@@ -73,3 +73,19 @@ def test_two_gloo_ranks_cover_the_batch_once():
     plans = P.build_plans([_scene(f)[1] for f in range(FRAMES)], _params(), "optimized", 2)
     assert blocks == sum(p.n_processed for p in plans)
     assert nframes == FRAMES
+
+
+def test_conceal_batch_chunk_bounds(monkeypatch):
+    """conceal_batch's staged pipeline covers every frame exactly once, in order."""
+    from paper_2207_00233_b200.conceal import _chunk_bounds
+
+    for n in (1, 2, 3, 4, 5, 9, 16, 63, 64, 100):
+        b = _chunk_bounds(n)
+        assert b[0] == 0 and b[-1] == n
+        assert all(x < y for x, y in zip(b, b[1:]))
+        assert len(b) == (2 if n < 4 else 3)
+    monkeypatch.setenv("FSE_CHUNKS", "0.0625,0.125,0.6875,0.125")
+    for n in (1, 5, 64):
+        b = _chunk_bounds(n)
+        assert b[0] == 0 and b[-1] == n and all(x < y for x, y in zip(b, b[1:]))
+    assert _chunk_bounds(64) == [0, 4, 12, 56, 64]
