@@ -387,14 +387,15 @@ def run_b200(a, rank, world, local_rank):
         pk = fp32_peak if precision == "fp32" else peaks["dfma"]
         tr, detail = None, None
         blocks_per_launch = blocks_rank * a.steps / max(1, m["level_launches"])
-        if traffic and precision == "fp32":
+        tp = traffic.get(precision) if traffic else None
+        if tp:
             # ncu dram bytes per window x the average windows of a timed launch
-            tr = traffic["dram_bytes_per_block"] * blocks_per_launch
-            detail = {"dram_bytes_per_block": traffic["dram_bytes_per_block"],
-                      "algorithmic_bytes_per_block": traffic["algorithmic_bytes_per_block"],
+            tr = tp["dram_bytes_per_block"] * blocks_per_launch
+            detail = {"dram_bytes_per_block": tp["dram_bytes_per_block"],
+                      "algorithmic_bytes_per_block": tp["algorithmic_bytes_per_block"],
                       "avg_blocks_per_launch": blocks_per_launch,
-                      "profiled_launch": {"blocks": traffic["launch_blocks"],
-                                          "dram_bytes": traffic["dram_bytes_per_launch"]},
+                      "profiled_launch": {"blocks": tp["launch_blocks"],
+                                          "dram_bytes": tp["dram_bytes_per_launch"]},
                       "source": traffic["source"]}
         return {"bound": "fp32" if precision == "fp32" else "fp64", "achieved": achieved, "peak": pk,
                 "unit": "TFLOP/s", "frac": achieved / pk, "frac_of_fp32_peak": achieved / fp32_peak,
