@@ -600,14 +600,21 @@ def run_strips_bench(a, rank, world, local_rank):
                                                Bk, H, dist, grp)
         stats["levels"] = ex.n_levels
         ex.close()
-        if world > 1:  # gather the bands to rank 0
+        if world > 1:  # gather the bands to rank 0 (gloo: through host buffers)
             lo, hi = bands[rank]
+            host = dist.get_backend() == "gloo"
             if rank == 0:
                 for r in range(1, world):
                     y0, y1 = bands[r][0] * Bk, min(H, bands[r][1] * Bk)
-                    dist.recv(work[y0:y1], r)
+                    if host:
+                        hb = work[y0:y1].cpu()
+                        dist.recv(hb, r)
+                        work[y0:y1].copy_(hb)
+                    else:
+                        dist.recv(work[y0:y1], r)
             else:
-                dist.send(work[lo * Bk:min(H, hi * Bk)].contiguous(), 0)
+                rows = work[lo * Bk:min(H, hi * Bk)].contiguous()
+                dist.send(rows.cpu() if host else rows, 0)
         return plan
 
     for _ in range(a.warmup):
@@ -630,6 +637,15 @@ def run_strips_bench(a, rank, world, local_rank):
     if world > 1:
         ms = _allreduce(torch, dist, [ms], dist.ReduceOp.MAX)[0]
     launches = int(lib.fse_launch_count(1))
+    strips_equal = None
+    if world > 1 and rank == 0:
+        # the gathered strip-sharded frame against one whole-frame run on this
+        # GPU (same kernels; untimed)
+        whole = src.clone()
+        wout = torch.empty_like(msk)
+        P.run_frames_device([P.build_plan(mask, params)], [whole], [msk], [wout], params, "fp32")
+        torch.cuda.synchronize()
+        strips_equal = bool(torch.equal(whole, work))
     if rank == 0:
         blocks = stats["blocks"]
         flop = counted_flops_per_block(100, Fk, Fk) * blocks
@@ -648,6 +664,8 @@ def run_strips_bench(a, rank, world, local_rank):
             "counted_tflop_per_s": flop * a.steps / (ms * 1e-3) / 1e12,
             "gpu_launches": launches, "clocks": clk.summary(),
         }
+        if strips_equal is not None:
+            line["strips_equal_whole_frame"] = strips_equal
         print(json.dumps(line), flush=True)
 
 

@@ -100,10 +100,21 @@ def run_levels(executor, image, rank: int, world: int, bands, flags_all, n_level
         sends, recvs = exchange_plan(rank, world, bands, flags_all, l, R, B, H)
         if not sends and not recvs:
             continue
-        ops = [dist.P2POp(dist.isend, image[y0:y1], peer, group) for peer, y0, y1 in sends]
-        ops += [dist.P2POp(dist.irecv, image[y0:y1], peer, group) for peer, y0, y1 in recvs]
-        for w in dist.batch_isend_irecv(ops):
-            w.wait()
+        if getattr(image, "is_cuda", False) and dist.get_backend(group) == "gloo":
+            # gloo moves host memory only: stage the halo rows through the host
+            # (functional runs of several ranks on one GPU; NCCL sends in place)
+            rbufs = [(image[y0:y1], image[y0:y1].cpu()) for _, y0, y1 in recvs]
+            ops = [dist.P2POp(dist.isend, image[y0:y1].cpu(), peer, group) for peer, y0, y1 in sends]
+            ops += [dist.P2POp(dist.irecv, hb, peer, group) for (peer, _, _), (_, hb) in zip(recvs, rbufs)]
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+            for dv, hb in rbufs:
+                dv.copy_(hb)
+        else:
+            ops = [dist.P2POp(dist.isend, image[y0:y1], peer, group) for peer, y0, y1 in sends]
+            ops += [dist.P2POp(dist.irecv, image[y0:y1], peer, group) for peer, y0, y1 in recvs]
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
         sent += len(sends)
     return sent
 
