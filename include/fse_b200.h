@@ -162,6 +162,14 @@ int fse_set_dataflow(int32_t on);
  * another group's work.  1..8, default 2 (FSE_GROUPS sets the default).
  * Results are identical for every n.  Process-wide. */
 int fse_set_groups(int32_t n);
+/* fp32 argmax form per level launch: launches of fewer windows than this use
+ * the tracked argmax (each thread carries its best bin; one barrier per
+ * iteration), wider ones the lazy argmax (running maximum only; the winning
+ * warp re-finds its bin after a second barrier).  Same argmax, identical
+ * results; tracked is faster on narrow (latency-bound) levels.  Default
+ * 16 x SM count (FSE_TRACK_BELOW sets the default); 0 = always lazy.
+ * Process-wide. */
+int fse_set_track_below(int32_t windows);
 /* Windows redone in fp64 by the guard, summed over timed calls (fse_timing_*). */
 int64_t fse_guard_redo_count(int32_t reset);
 

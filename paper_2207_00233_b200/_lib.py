@@ -21,7 +21,7 @@ EXPORTS = (
     "fse_plan_free", "fse_plan_sizes", "fse_plan_batches", "fse_plan_levels", "fse_plan_ranks",
     "fse_plan_unconcealed", "fse_init_counts", "fse_schedule_all", "fse_conceal_frames",
     "fse_launch_count", "fse_timing_enable", "fse_timing_read", "fse_fma_probe",
-    "fse_set_guard", "fse_guard_redo_count", "fse_set_dataflow", "fse_set_groups",
+    "fse_set_guard", "fse_guard_redo_count", "fse_set_dataflow", "fse_set_groups", "fse_set_track_below",
     "fse_shard_open", "fse_shard_levels", "fse_shard_run", "fse_shard_close",
     "fse_quantize_psnr",
 )
@@ -88,6 +88,7 @@ def lib():
         L.fse_guard_redo_count.argtypes = [_i32]
         L.fse_set_dataflow.argtypes = [_i32]
         L.fse_set_groups.argtypes = [_i32]
+        L.fse_set_track_below.argtypes = [_i32]
         L.fse_shard_open.argtypes = [_vp, _i32, _i32, _vp, _vp, _vp, ctypes.POINTER(FseParamsC), _i32,
                                      _vp, _i32, _vp, ctypes.POINTER(_vp)]
         L.fse_shard_levels.argtypes = [_vp, _pi32, _pi32]

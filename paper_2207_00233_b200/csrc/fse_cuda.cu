@@ -3,6 +3,8 @@
 // kernel in fse_kernel.cuh).  See include/fse_b200.h for the ABI.
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include <algorithm>
 #include <mutex>
 #include <cstdlib>
@@ -238,6 +240,10 @@ int dispatch(const KArgs &a, int grid, int Mmax, int Nmax, int F1, int F2, int m
 
 using fse::fail;
 
+namespace fse {
+extern std::atomic<int> g_track_below;  // fse_inst_fast.cu
+}
+
 extern "C" {
 
 int fse_version(int32_t *out, int32_t n) {
@@ -336,6 +342,12 @@ int fse_set_guard(double tau0, double tau1) {
 
 int fse_set_dataflow(int32_t on) {
     fse::g_dataflow = on != 0;
+    return FSE_OK;
+}
+
+int fse_set_track_below(int32_t windows) {
+    if (windows < 0) return fail(FSE_EINVAL, "track_below must be >= 0");
+    fse::g_track_below.store(windows, std::memory_order_relaxed);
     return FSE_OK;
 }
 

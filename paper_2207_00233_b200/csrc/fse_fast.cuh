@@ -37,8 +37,14 @@
 
 namespace fse {
 
-template <typename T_, int F_, int NW_, bool EXT_ = true, int MINB_ = 0, int CL_ = 1>
+template <typename T_, int F_, int NW_, bool EXT_ = true, int MINB_ = 0, int CL_ = 1, bool TRACK_ = false>
 struct FastCfg {
+    // TRACK (fp32): every thread carries its best bin (index, g) through the
+    // update and the argmax takes one barrier; otherwise fp32 uses the lazy
+    // argmax (running maximum only, candidate warps re-find their bin after a
+    // second barrier).  Lazy is faster on wide levels (issue-bound), tracked on
+    // levels narrower than a few waves (latency-bound).
+    static constexpr bool TRACK = TRACK_;
     static constexpr int MINB = MINB_;  // __launch_bounds__ min blocks per SM (0 = unspecified)
     // CL > 1: one window is split over a thread-block cluster of CL CTAs (one
     // per SM): the bins are spread over CL * NW warps, every CTA keeps a full
@@ -643,7 +649,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     // LAZY: only the running maximum energy is kept per bin (one FMNMX); the
     // few lanes holding the CTA maximum find its bin again after the reduction
     // (a second barrier), instead of every bin carrying index and g along.
-    constexpr bool LAZY = IS_F32 && CL == 1 && !GUARD;
+    constexpr bool LAZY = IS_F32 && CL == 1 && !GUARD && !C::TRACK;
     T tmax = (T)0;
     using KeyT = decltype(energy_key((T)0));
     auto track = [&](int j, T e) {

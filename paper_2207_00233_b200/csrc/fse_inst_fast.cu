@@ -1,4 +1,5 @@
 // Instantiation + host launchers of the fast-path kernel (fse_fast.cuh).
+#include <atomic>
 #include <cstdlib>
 #include <algorithm>
 #include <string>
@@ -16,6 +17,27 @@ namespace fse {
 template <typename T> using Fast64 = FastCfg<T, 64, 6, sizeof(T) == 4, sizeof(T) == 4 ? 4 : 3>;  // fp64: plain W plane
 
 template <typename T> using Fast32 = FastCfg<T, 32, 6>;
+// tracked-argmax fp32 twins for narrow levels (see FastCfg::TRACK)
+using Fast64T = FastCfg<float, 64, 6, true, 4, 1, true>;
+using Fast32T = FastCfg<float, 32, 6, true, 0, 1, true>;
+
+// Levels narrower than this many windows use the tracked argmax (fp32):
+// measured on configs 2 (linescan), 3 and 5 -- levels of a few hundred
+// windows -- 3-10% faster, on config 4's levels of thousands 1% slower.
+// Default 16 x SMs; FSE_TRACK_BELOW or fse_set_track_below override (0 = never).
+// Both forms compute the same argmax, so results are identical.
+std::atomic<int> g_track_below{-1};
+static int track_below(int sms) {
+    int v = g_track_below.load(std::memory_order_relaxed);
+    if (v < 0) {
+        const char *e = getenv("FSE_TRACK_BELOW");
+        v = e ? atoi(e) : 16 * sms;
+        int expect = -1;
+        g_track_below.compare_exchange_strong(expect, v);
+        v = g_track_below.load(std::memory_order_relaxed);
+    }
+    return v;
+}
 // F = 128 (fp32 only: the row-extended W plane is 193 x 128 x 8 B = 198 KB):
 // 260 row segments over 20 warps -> 13 bins per thread, one CTA per SM.
 template <typename T> using Fast128 = FastCfg<T, 128, 20>;
@@ -180,11 +202,15 @@ int fast_level(int dtype, int F, bool guard, const FastArgs &a, int grid, int Mm
     }
     if (dtype == FSE_F32) {
         if (F == 128) return launch<Fast128<float>, 0, false>(a, grid, Mmax, Nmax, model_n, s);
-        if (F == 64)
-            return guard ? launch<Fast64<float>, 0, true>(a, grid, Mmax, Nmax, model_n, s)
-                         : launch<Fast64<float>, 0, false>(a, grid, Mmax, Nmax, model_n, s);
-        return guard ? launch<Fast32<float>, 0, true>(a, grid, Mmax, Nmax, model_n, s)
-                     : launch<Fast32<float>, 0, false>(a, grid, Mmax, Nmax, model_n, s);
+        const bool narrow = grid < track_below(sms);
+        if (F == 64) {
+            if (guard) return launch<Fast64<float>, 0, true>(a, grid, Mmax, Nmax, model_n, s);
+            return narrow ? launch<Fast64T, 0, false>(a, grid, Mmax, Nmax, model_n, s)
+                          : launch<Fast64<float>, 0, false>(a, grid, Mmax, Nmax, model_n, s);
+        }
+        if (guard) return launch<Fast32<float>, 0, true>(a, grid, Mmax, Nmax, model_n, s);
+        return narrow ? launch<Fast32T, 0, false>(a, grid, Mmax, Nmax, model_n, s)
+                      : launch<Fast32<float>, 0, false>(a, grid, Mmax, Nmax, model_n, s);
     }
     if (F == 64) return launch<Fast64<double>, 0, false>(a, grid, Mmax, Nmax, model_n, s);
     return launch<Fast32<double>, 0, false>(a, grid, Mmax, Nmax, model_n, s);

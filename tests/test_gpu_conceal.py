@@ -504,3 +504,27 @@ def test_fp32_guard_redo_everything_matches_fp64():
     assert redone == rep.blocks_processed
     np.testing.assert_array_equal(m32, m64)
     assert np.max(np.abs(g32 - o64)) <= 1e-3
+
+
+@pytest.mark.parametrize("cfg,B,F", [(3, 4, 64), (5, 2, 32)])
+def test_tracked_and_lazy_argmax_identical(cfg, B, F):
+    """fp32 level launches pick the argmax form by width (fse_set_track_below):
+    the tracked form (best bin carried per thread, one barrier) and the lazy
+    form (running maximum, second barrier) find the same first maximum, so the
+    frames are bit-identical."""
+    from paper_2207_00233_b200 import _lib
+
+    img, mask = synth.config_scene(cfg)
+    img, mask = img[:192, :320].copy(), mask[:192, :320].copy()
+    p = P.FseParams(d=14, iterations=60, block_size=B, fft_size=F)
+    L = _lib.lib()
+    outs = []
+    try:
+        for below in (1 << 30, 0):  # always tracked, always lazy
+            assert L.fse_set_track_below(below) == 0
+            o, m, _ = P.conceal(img, mask, p, precision="fp32")
+            outs.append((o.tobytes(), m.tobytes()))
+    finally:
+        L.fse_set_track_below(148 * 16)
+    assert outs[0] == outs[1]
+    assert L.fse_set_track_below(-1) != 0
