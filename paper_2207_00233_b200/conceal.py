@@ -363,10 +363,14 @@ def conceal_batch(images, masks, params: FseParams | None = None, order: str = O
         out_msk[lo:hi].copy_(out_d[lo:hi], non_blocking=True)
 
     trace = [("start", time.perf_counter())] if _TRACE else None
+    dev_ev = [] if _TRACE else None  # (label, event on the main stream)
 
     def mark(what):
         if trace is not None:
             trace.append((what, time.perf_counter()))
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(main)
+            dev_ev.append((what, ev))
 
     # chunk 0 is uploaded on the main stream; the rest on the copy stream while
     # chunk 0 computes.  Each chunk is planned while the previous one computes;
@@ -404,6 +408,10 @@ def conceal_batch(images, masks, params: FseParams | None = None, order: str = O
     if trace is not None:
         print("conceal_batch: " + "  ".join(f"{w} {1e3 * (t - trace[i][1]):.1f}"
                                             for i, (w, t) in enumerate(trace[1:])), flush=True)
+        # device time between the marks (main stream): what the GPU spent on
+        # each stage, as opposed to the host's enqueue time above
+        print("  device: " + "  ".join(f"{w} {dev_ev[i][1].elapsed_time(e):.1f}"
+                                       for i, (w, e) in enumerate(dev_ev[1:])), flush=True)
     wall = time.perf_counter() - t0
     reps = [_report(p, order, 1, wall) for p in plans] if reports else None
     return out_img.numpy(), out_msk.numpy(), reps

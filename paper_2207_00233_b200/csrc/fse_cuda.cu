@@ -68,6 +68,41 @@ struct PinnedStage {
 static std::mutex g_stage_mu;
 static std::vector<PinnedStage> g_stage;
 
+// Device staging of the sessions comes from a library-owned stream-ordered
+// pool that keeps freed memory (release threshold = max): with the default
+// pool (threshold 0) every synchronisation point hands the previous call's
+// staging back to the OS, and that unmapping runs inside the caller's
+// cudaStreamSynchronize after the GPU is already done (measured: 100-800 ms
+// stalls on one conceal_batch call in five).
+static cudaMemPool_t staging_pool() {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!pools[dev]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t p = nullptr;
+        if (cudaMemPoolCreate(&p, &props) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
+        pools[dev] = p;
+    }
+    return pools[dev];
+}
+
+static cudaError_t staging_alloc(void **p, size_t bytes, cudaStream_t s) {
+    cudaMemPool_t pool = staging_pool();
+    return pool ? cudaMallocFromPoolAsync(p, bytes, pool, s) : cudaMallocAsync(p, bytes, s);
+}
+
 static int stage_acquire(size_t bytes, int *slot, unsigned char **ptr) {
     // the smallest idle buffer that fits; otherwise a new one.  Buffers are
     // never freed here: cudaFreeHost would synchronise the device and drain
@@ -539,7 +574,7 @@ static int session_open(int32_t n, FsePlan *const *plans, void *const *images, c
         delete S;
         return rc;
     }
-    cudaError_t ce = cudaMallocAsync((void **)&S->dev, bytes, s);
+    cudaError_t ce = staging_alloc((void **)&S->dev, bytes, s);
     if (ce != cudaSuccess) {
         stage_release(slot, s);
         delete S;
