@@ -194,10 +194,11 @@ def test_all_lost_and_retry_sweeps():
     assert len(seen) == len(set(seen)) == 64
 
 
-@pytest.mark.parametrize("nf", [3, 9])
+@pytest.mark.parametrize("nf", [3, 9, 17])
 def test_conceal_batch_equals_per_frame(nf):
     """One-chunk batches (< 4 frames) and the staged pipeline (first chunk, the
-    rest uploaded and downloaded on the copy stream) equal per-frame conceal."""
+    rest uploaded and downloaded on the copy stream; a third, small chunk from
+    16 frames on) equal per-frame conceal."""
     import torch
 
     frames = [synth.synthetic_frame(96, 160, 50 + f, 6, 3) for f in range(nf)]

@@ -83,7 +83,7 @@ def test_conceal_batch_chunk_bounds(monkeypatch):
         b = _chunk_bounds(n)
         assert b[0] == 0 and b[-1] == n
         assert all(x < y for x, y in zip(b, b[1:]))
-        assert len(b) == (2 if n < 4 else 3)
+        assert len(b) == (2 if n < 4 else 3 if n < 16 else 4)
     monkeypatch.setenv("FSE_CHUNKS", "0.0625,0.125,0.6875,0.125")
     for n in (1, 5, 64):
         b = _chunk_bounds(n)
