@@ -61,6 +61,9 @@ def args_():
     ap.add_argument("--frames", type=int, default=64)
     ap.add_argument("--guard", default=None,
                     help="fp32 near-tie guard 'tau0,tau1' or 'off' (default: library default)")
+    ap.add_argument("--halo", default="p2p", choices=["p2p", "collective"],
+                    help="config 5 at N>1: fused halo stores over peer memory (default) or per-level "
+                         "send/recv over torch.distributed")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-second", action="store_true", help="skip the other precision's measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -579,6 +582,9 @@ def run_strips_bench(a, rank, world, local_rank):
     R = strips.halo_rows(params)
     grp = dist.group.WORLD if world > 1 else None
     stats = {}
+    # fused halo exchange: the frame buffer is fixed, so its peer mappings are
+    # set up once; each step is a new epoch of the device flags
+    link = strips.PeerLink(work, rank, world, dist, grp) if world > 1 and a.halo == "p2p" else None
 
     def step():
         work.copy_(src)
@@ -589,15 +595,19 @@ def run_strips_bench(a, rank, world, local_rank):
         stats["plan_ms"] = 1e3 * (time.perf_counter() - t0)
         stats["blocks"] = plan.n_processed
         ex = strips.ShardExecutor(plan, bands[rank], work, msk, out, params, "fp32")
-        flags_all = [ex.flags]
-        if world > 1:
-            dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
-            t = torch.as_tensor(ex.flags, dtype=torch.int32, device=dev)
-            g = [torch.empty_like(t) for _ in range(world)]
-            dist.all_gather(g, t)
-            flags_all = [x.cpu().numpy() for x in g]
-        stats["halo_msgs"] = strips.run_levels(ex, work, rank, world, bands, flags_all, ex.n_levels, R,
-                                               Bk, H, dist, grp)
+        if link is not None:
+            strips.run_levels_p2p(ex, link)
+            stats["halo_msgs"] = 0
+        else:
+            flags_all = [ex.flags]
+            if world > 1:
+                dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+                t = torch.as_tensor(ex.flags, dtype=torch.int32, device=dev)
+                g = [torch.empty_like(t) for _ in range(world)]
+                dist.all_gather(g, t)
+                flags_all = [x.cpu().numpy() for x in g]
+            stats["halo_msgs"] = strips.run_levels(ex, work, rank, world, bands, flags_all, ex.n_levels, R,
+                                                   Bk, H, dist, grp)
         stats["levels"] = ex.n_levels
         ex.close()
         if world > 1:  # gather the bands to rank 0 (gloo: through host buffers)
@@ -657,7 +667,9 @@ def run_strips_bench(a, rank, world, local_rank):
             "config": {"workload": f"config5: 3840x2160 synthetic luma, 50% burst 16x16 losses, FSE "
                                    f"{Bk}x{Bk} / d=14 / FFT {Fk}x{Fk} / 100 it, optimized order, fp32, "
                                    f"strip-sharded", "block": Bk, "fft": Fk,
-                       "parallelism": f"row bands x{world}, per-level halo exchange"},
+                       "parallelism": f"row bands x{world}, halo exchange: "
+                                      + ("fused peer stores + device flags" if link is not None
+                                         else "per-level send/recv" if world > 1 else "none")},
             "lost_mpixel_per_s": float((mask == 1).sum()) * a.steps / (ms * 1e-3) / 1e6,
             "blocks_per_step": blocks, "levels_per_step": stats["levels"],
             "host_plan_ms_per_step": stats["plan_ms"], "halo_messages_rank0": stats["halo_msgs"],
@@ -667,6 +679,10 @@ def run_strips_bench(a, rank, world, local_rank):
         if strips_equal is not None:
             line["strips_equal_whole_frame"] = strips_equal
         print(json.dumps(line), flush=True)
+    if link is not None:
+        torch.cuda.synchronize()
+        dist.barrier()
+        link.close()
 
 
 def main():

@@ -195,6 +195,33 @@ int fse_shard_run(FseShard *shard, int32_t level_lo, int32_t level_hi, void *str
 /* mask pass over the band's rows (if mask_out was given) and release */
 int fse_shard_close(FseShard *shard, void *stream);
 
+/* Fused halo exchange over peer memory (NVLink / NVSwitch), replacing the
+ * per-level NCCL send/recv of the protocol above: the level kernel's
+ * write-back also stores the band-edge blocks (block rows within R of the
+ * edge) straight into the neighbour's frame, and per level the shard signals
+ * the neighbours through device flags; before level l its stream waits (a
+ * front-end cuStreamWaitValue32, no spinning SM) until both neighbours have
+ * completed level l-1, and after the last level until they are done writing
+ * into this frame.  The whole level sequence is then one fse_shard_run call
+ * with no host round trips.  Peer frames and flags are CUDA IPC mappings
+ * (one process per GPU).  Same results as the NCCL protocol.
+ * Handles are FSE_IPC_HANDLE_BYTES opaque bytes (allocation handle + offset). */
+#define FSE_IPC_HANDLE_BYTES 72
+int fse_ipc_handle(const void *dev_ptr, void *handle);
+int fse_ipc_open(const void *handle, void **dev_ptr);
+int fse_ipc_close(void *dev_ptr);
+/* two zeroed uint32 device flags: [0] from the upper neighbour, [1] from the lower */
+int fse_flags_alloc(uint32_t **flags);
+int fse_flags_free(uint32_t *flags);
+/* neighbours' frames and flags (NULL = no neighbour on that side), this
+ * rank's own flags, and the run's epoch (1, 2, 3, ... identical on every
+ * rank; flag values of one epoch never satisfy another's waits).  A run
+ * starting at level 0 first signals "frame initialised" and waits for the
+ * neighbours' signal, so work queued before it on the stream (a frame reset)
+ * precedes every peer store into this frame. */
+int fse_shard_set_peers(FseShard *shard, void *up_image, uint32_t *up_flags, void *down_image,
+                        uint32_t *down_flags, uint32_t *own_flags, uint32_t epoch);
+
 /* Output epilogue over n frames of npix samples each (device pointers, frames
  * contiguous): out_u8 (or NULL) = floor(clip(x, 0, 255) + 0.5), the rounding
  * of fsefill.image.save_pgm (image.py:79-88); if sums != NULL, per frame f

@@ -15,6 +15,7 @@ LIB_PATH = os.environ.get("FSE_LIB") or os.path.join(_HERE, "libfse_b200.so")
 FSE_OK, FSE_EINVAL, FSE_ENOMEM, FSE_ECUDA, FSE_ENOTSUP = 0, -22, -12, -5, -95
 FSE_F64, FSE_F32 = 0, 1
 FSE_ORDER_OPTIMIZED, FSE_ORDER_LINESCAN = 0, 1
+FSE_IPC_HANDLE_BYTES = 72
 
 EXPORTS = (
     "fse_last_error", "fse_version", "fse_run_windows", "fse_plan_build", "fse_plan_build_many",
@@ -23,7 +24,8 @@ EXPORTS = (
     "fse_launch_count", "fse_timing_enable", "fse_timing_read", "fse_fma_probe",
     "fse_set_guard", "fse_guard_redo_count", "fse_set_dataflow", "fse_set_groups", "fse_set_track_below",
     "fse_shard_open", "fse_shard_levels", "fse_shard_run", "fse_shard_close",
-    "fse_quantize_psnr",
+    "fse_ipc_handle", "fse_ipc_open", "fse_ipc_close", "fse_flags_alloc", "fse_flags_free",
+    "fse_shard_set_peers", "fse_quantize_psnr",
 )
 
 
@@ -94,6 +96,12 @@ def lib():
         L.fse_shard_levels.argtypes = [_vp, _pi32, _pi32]
         L.fse_shard_run.argtypes = [_vp, _i32, _i32, _vp]
         L.fse_shard_close.argtypes = [_vp, _vp]
+        L.fse_ipc_handle.argtypes = [_vp, _vp]
+        L.fse_ipc_open.argtypes = [_vp, ctypes.POINTER(_vp)]
+        L.fse_ipc_close.argtypes = [_vp]
+        L.fse_flags_alloc.argtypes = [ctypes.POINTER(_vp)]
+        L.fse_flags_free.argtypes = [_vp]
+        L.fse_shard_set_peers.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_uint32]
         L.fse_quantize_psnr.argtypes = [_i32, ctypes.c_int64, _vp, _i32, _vp, _vp, _vp, _vp, _vp]
         L.fse_guard_redo_count.restype = ctypes.c_int64
         L.fse_launch_count.argtypes = [_i32]

@@ -468,6 +468,12 @@ struct FseShard {
     bool fast = false, guard = false, masks_out = false;
     fse::KArgs a{};
     fse::FastArgs f{};
+    // fused halo exchange (fse_shard_set_peers): flag words this shard signals
+    // (the upper neighbour's "from below", the lower neighbour's "from above"),
+    // its own two flags, and the epoch base of the flag values
+    uint32_t *sig_up = nullptr, *sig_down = nullptr, *own_flags = nullptr;
+    uint32_t base = 0;
+    bool peers = false;
 };
 
 namespace fse {
@@ -653,6 +659,66 @@ static int session_open(int32_t n, FsePlan *const *plans, void *const *images, c
     return FSE_OK;
 }
 
+// ---- fused halo exchange: cross-device flags ------------------------------
+// A level's peer stores are made visible (__threadfence_system in the level
+// kernel), then this one-thread kernel release-stores the level count into
+// the neighbours' flag words (peer memory).  The neighbour's stream waits on
+// its own flag word with cuStreamWaitValue32 (a front-end wait: no SM spins).
+static __global__ void peer_signal_kernel(uint32_t *a, uint32_t *b, uint32_t v) {
+    __threadfence_system();
+    if (a) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+    if (b) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(b), "r"(v) : "memory");
+}
+
+// fallback when the driver entry point is unavailable: one thread polls
+static __global__ void peer_wait_kernel(const uint32_t *f, uint32_t v) {
+    uint32_t x;
+    for (;;) {
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(x) : "l"(f) : "memory");
+        if ((int32_t)(x - v) >= 0) break;
+        __nanosleep(200);
+    }
+}
+
+typedef int (*StreamWaitValue32Fn)(void *stream, unsigned long long addr, uint32_t value, unsigned int flags);
+static StreamWaitValue32Fn stream_wait_fn(unsigned int *flags) {
+    static StreamWaitValue32Fn fn = nullptr;
+    static unsigned int fl = 0;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<StreamWaitValue32Fn>(p);
+        else
+            cudaGetLastError();
+        // CU_STREAM_WAIT_VALUE_GEQ (0) | CU_STREAM_WAIT_VALUE_FLUSH (1 << 30) where the
+        // device can flush remote writes (CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES = 98)
+        typedef int (*DevAttrFn)(int *, int, int);
+        void *pa = nullptr;
+        int dev = 0, can = 0;
+        if (cudaGetDriverEntryPoint("cuDeviceGetAttribute", &pa, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess && cudaGetDevice(&dev) == cudaSuccess &&
+            reinterpret_cast<DevAttrFn>(pa)(&can, 98, dev) == 0 && can)
+            fl = 1u << 30;
+        cudaGetLastError();
+    });
+    *flags = fl;
+    return fn;
+}
+
+static int peer_wait(const uint32_t *flag, uint32_t v, cudaStream_t s) {
+    unsigned int fl = 0;
+    if (StreamWaitValue32Fn fn = stream_wait_fn(&fl)) {
+        if (fn(s, (unsigned long long)(uintptr_t)flag, v, fl) != 0) return fail(FSE_ECUDA, "cuStreamWaitValue32");
+        return FSE_OK;
+    }
+    peer_wait_kernel<<<1, 1, 0, s>>>(flag, v);
+    const cudaError_t ce = cudaGetLastError();
+    return ce == cudaSuccess ? FSE_OK : fail(FSE_ECUDA, std::string("peer wait: ") + cudaGetErrorString(ce));
+}
+
 // Launch levels [l0, l1).  `whole` allows the dataflow executor (all levels at once).
 static int session_run(FseShard *S, int l0, int l1, bool whole, cudaStream_t s) {
     l0 = std::max(0, l0);
@@ -696,6 +762,48 @@ static int session_run(FseShard *S, int l0, int l1, bool whole, cudaStream_t s) 
             if (!gs[g]) return fail(FSE_ECUDA, "group stream");
             cudaStreamWaitEvent(gs[g], gev[G], 0);
         }
+    }
+    if (S->peers) {
+        // fused halo exchange: per level, wait for the neighbours' previous
+        // level, launch (peer stores in the write-back), signal the neighbours.
+        // Flag values of epoch e lie in [base, base + n_levels]: base = "this
+        // frame is initialised for epoch e" (signalled after whatever the
+        // caller queued before, e.g. the frame reset), base + l = "levels
+        // 0..l-1 done".  Level 0 waits for the neighbours' base, so no peer
+        // store of this epoch can land before the neighbour's reset.
+        if (l0 == 0 && l1 > l0) {
+            peer_signal_kernel<<<1, 1, 0, s>>>(S->sig_up, S->sig_down, S->base);
+            const cudaError_t ce = cudaGetLastError();
+            if (ce != cudaSuccess) rc = fail(FSE_ECUDA, std::string("peer signal: ") + cudaGetErrorString(ce));
+            if (rc == FSE_OK && S->sig_up) rc = peer_wait(S->own_flags + 0, S->base, s);
+            if (rc == FSE_OK && S->sig_down) rc = peer_wait(S->own_flags + 1, S->base, s);
+        }
+        for (int l = l0; l < l1 && rc == FSE_OK; ++l) {
+            if (l > 0) {
+                if (S->sig_up) rc = peer_wait(S->own_flags + 0, S->base + (uint32_t)l, s);
+                if (rc == FSE_OK && S->sig_down) rc = peer_wait(S->own_flags + 1, S->base + (uint32_t)l, s);
+            }
+            const int2 *lvl = reinterpret_cast<const int2 *>(dev + S->off_ent) + S->lvl_off[l];
+            const int cnt = S->lvl_off[l + 1] - S->lvl_off[l];
+            if (rc == FSE_OK && cnt > 0) {
+                f.entries = lvl;
+                f.redo_list = redo + S->lvl_off[l];
+                f.redo_count = counters + l;
+                rc = fast_level(S->dtype, S->F1, false, f, cnt, S->Mmax, S->Nmax, S->model_n, s);
+                if (g_timing.on) ++g_timing.window_launches;
+            }
+            if (rc == FSE_OK) {
+                peer_signal_kernel<<<1, 1, 0, s>>>(S->sig_up, S->sig_down, S->base + (uint32_t)l + 1);
+                const cudaError_t ce = cudaGetLastError();
+                if (ce != cudaSuccess) rc = fail(FSE_ECUDA, std::string("peer signal: ") + cudaGetErrorString(ce));
+            }
+        }
+        // after the last level: the neighbours are done writing into this frame
+        if (rc == FSE_OK && l1 == S->n_levels && l1 > l0) {
+            if (S->sig_up) rc = peer_wait(S->own_flags + 0, S->base + (uint32_t)S->n_levels, s);
+            if (rc == FSE_OK && S->sig_down) rc = peer_wait(S->own_flags + 1, S->base + (uint32_t)S->n_levels, s);
+        }
+        l1 = l0;  // nothing left for the generic loop below
     }
     for (int l = l0; l < l1 && rc == FSE_OK; ++l)
         for (int g = 0; g < G && rc == FSE_OK; ++g) {
@@ -811,6 +919,105 @@ int fse_shard_levels(const FseShard *sh, int32_t *n_levels, int32_t *edge_flags)
 int fse_shard_run(FseShard *sh, int32_t level_lo, int32_t level_hi, void *stream) {
     if (!sh) return fail(FSE_EINVAL, "NULL shard");
     return fse::session_run(sh, level_lo, level_hi, false, (cudaStream_t)stream);
+}
+
+int fse_ipc_handle(const void *dev_ptr, void *handle) {
+    if (!dev_ptr || !handle) return fail(FSE_EINVAL, "NULL argument");
+    // IPC handles name whole allocations: export the base, carry the offset
+    typedef int (*RangeFn)(unsigned long long *, size_t *, unsigned long long);
+    static RangeFn range = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            return (RangeFn) nullptr;
+        }
+        return reinterpret_cast<RangeFn>(p);
+    }();
+    if (!range) return fail(FSE_ENOTSUP, "cuMemGetAddressRange unavailable");
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (range(&base, &size, (unsigned long long)(uintptr_t)dev_ptr) != 0)
+        return fail(FSE_EINVAL, "not a device allocation");
+    cudaIpcMemHandle_t h;
+    const cudaError_t ce = cudaIpcGetMemHandle(&h, (void *)(uintptr_t)base);
+    if (ce != cudaSuccess) return fail(FSE_ECUDA, std::string("ipc handle: ") + cudaGetErrorString(ce));
+    const unsigned long long off = (unsigned long long)(uintptr_t)dev_ptr - base;
+    std::memcpy(handle, &h, sizeof(h));
+    std::memcpy(static_cast<unsigned char *>(handle) + sizeof(h), &off, sizeof(off));
+    return FSE_OK;
+}
+
+static std::mutex g_ipc_mu;
+static std::vector<std::pair<void *, void *>> g_ipc_open;  // (returned pointer, mapped base)
+
+int fse_ipc_open(const void *handle, void **dev_ptr) {
+    if (!handle || !dev_ptr) return fail(FSE_EINVAL, "NULL argument");
+    cudaIpcMemHandle_t h;
+    unsigned long long off = 0;
+    std::memcpy(&h, handle, sizeof(h));
+    std::memcpy(&off, static_cast<const unsigned char *>(handle) + sizeof(h), sizeof(off));
+    void *base = nullptr;
+    const cudaError_t ce = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+    if (ce != cudaSuccess) return fail(FSE_ECUDA, std::string("ipc open: ") + cudaGetErrorString(ce));
+    *dev_ptr = static_cast<unsigned char *>(base) + off;
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    g_ipc_open.emplace_back(*dev_ptr, base);
+    return FSE_OK;
+}
+
+int fse_ipc_close(void *dev_ptr) {
+    void *base = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_ipc_mu);
+        for (size_t i = 0; i < g_ipc_open.size(); ++i)
+            if (g_ipc_open[i].first == dev_ptr) {
+                base = g_ipc_open[i].second;
+                g_ipc_open.erase(g_ipc_open.begin() + (long)i);
+                break;
+            }
+    }
+    if (!base) return fail(FSE_EINVAL, "pointer was not opened by fse_ipc_open");
+    const cudaError_t ce = cudaIpcCloseMemHandle(base);
+    return ce == cudaSuccess ? FSE_OK : fail(FSE_ECUDA, std::string("ipc close: ") + cudaGetErrorString(ce));
+}
+
+int fse_flags_alloc(uint32_t **flags) {
+    if (!flags) return fail(FSE_EINVAL, "NULL argument");
+    // own allocation (exported whole through IPC), zeroed
+    cudaError_t ce = cudaMalloc((void **)flags, 256);
+    if (ce == cudaSuccess) ce = cudaMemset(*flags, 0, 256);
+    if (ce == cudaSuccess) ce = cudaDeviceSynchronize();
+    return ce == cudaSuccess ? FSE_OK : fail(FSE_ECUDA, std::string("flags: ") + cudaGetErrorString(ce));
+}
+
+int fse_flags_free(uint32_t *flags) {
+    const cudaError_t ce = cudaFree(flags);
+    return ce == cudaSuccess ? FSE_OK : fail(FSE_ECUDA, std::string("flags free: ") + cudaGetErrorString(ce));
+}
+
+int fse_shard_set_peers(FseShard *sh, void *up_image, uint32_t *up_flags, void *down_image,
+                        uint32_t *down_flags, uint32_t *own_flags, uint32_t epoch) {
+    if (!sh) return fail(FSE_EINVAL, "NULL shard");
+    if ((up_image == nullptr) != (up_flags == nullptr) || (down_image == nullptr) != (down_flags == nullptr))
+        return fail(FSE_EINVAL, "a neighbour needs both its frame and its flags");
+    if ((up_image || down_image) && !own_flags) return fail(FSE_EINVAL, "NULL own flags");
+    if (!sh->fast || sh->guard || sh->n != 1)
+        return fail(FSE_ENOTSUP, "fused halo exchange needs the fast kernel (F = 32/64/128), no guard, one frame");
+    if (up_image && sh->row_lo == 0) return fail(FSE_EINVAL, "band at the top has no upper neighbour");
+    if (down_image && sh->row_hi >= sh->rows) return fail(FSE_EINVAL, "band at the bottom has no lower neighbour");
+    sh->f.peer_up = up_image;
+    sh->f.peer_down = down_image;
+    sh->f.peer_up_end = sh->row_lo + sh->R;
+    sh->f.peer_down_begin = sh->row_hi - sh->R;
+    sh->sig_up = up_flags ? up_flags + 1 : nullptr;        // the upper neighbour's "from below"
+    sh->sig_down = down_flags ? down_flags + 0 : nullptr;  // the lower neighbour's "from above"
+    sh->own_flags = own_flags;
+    if (epoch == 0) return fail(FSE_EINVAL, "epochs start at 1 (flags start at 0)");
+    sh->base = epoch * (uint32_t)(sh->n_levels + 1);
+    sh->peers = up_image || down_image;
+    return FSE_OK;
 }
 
 int fse_shard_close(FseShard *sh, void *stream) {

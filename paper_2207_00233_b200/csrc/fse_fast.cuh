@@ -193,6 +193,13 @@ struct FastArgs {
     int *done;   // per (frame, block): outstanding dependency count
     int *queue;  // ready queue, total slots, -1 = not yet written
     int R;
+    // fused halo exchange (row-band shards over peer memory, MODE 0): the
+    // write-back also stores into the upper / lower neighbour's frame (the
+    // same coordinates, mapped through CUDA IPC) for blocks whose block row is
+    // < peer_up_end / >= peer_down_begin -- the rows the neighbour's windows
+    // read.  nullptr = no neighbour on that side.
+    void *peer_up, *peer_down;
+    int peer_up_end, peer_down_begin;
 };
 
 __device__ __forceinline__ unsigned warp_max_u32(unsigned v) { return __reduce_max_sync(0xffffffffu, v); }
@@ -927,9 +934,17 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
             return acc;
         };
         // write-back of the block's LOST samples (conceal.py:61-66)
+        const int brow = blk / A.cols;
+        IT *pu = (A.peer_up && brow < A.peer_up_end) ? reinterpret_cast<IT *>(A.peer_up) : nullptr;
+        IT *pd = (A.peer_down && brow >= A.peer_down_begin) ? reinterpret_cast<IT *>(A.peer_down) : nullptr;
         auto store = [&](int q, T val) {
             const size_t off = (size_t)(wr0 + br0 + q / bw) * A.W + (wc0 + bc0 + q % bw);
-            if (fd->mask[off] == FSE_LOST) img[off] = (IT)val;
+            if (fd->mask[off] == FSE_LOST) {
+                img[off] = (IT)val;
+                // halo rows straight into the neighbour's frame over NVLink
+                if (pu) pu[off] = (IT)val;
+                if (pd) pd[off] = (IT)val;
+            }
         };
         if (crank == 0) {  // the cluster's CTA 0 writes the block
             if (nsamp <= NT) {
@@ -945,6 +960,9 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
             } else {
                 for (int q = t; q < nsamp; q += NT) store(q, model(q, 0, 1));
             }
+            // peer stores visible system-wide before this kernel completes (the
+            // stream's next op signals the neighbour)
+            if (pu || pd) __threadfence_system();
         }
     }
     // keep this CTA's shared memory alive until the cluster is done with it

@@ -14,7 +14,10 @@ one batch (fsefill/conceal.py:146-153).
 The level loop and the exchange schedule are written against a small executor
 interface so the same protocol runs on GPUs (ShardExecutor, C ABI fse_shard_*,
 NCCL point-to-point) and, in tests, on CPU ranks over gloo with an emulated
-kernel.
+kernel.  The default GPU transport fuses the exchange into the kernel instead
+(PeerLink): band-edge blocks are stored straight into the neighbour's frame
+over NVLink and levels are ordered by device flags, so a shard's whole level
+sequence is one call.
 """
 
 from __future__ import annotations
@@ -153,11 +156,71 @@ class ShardExecutor:
             self.handle = None
 
 
+class PeerLink:
+    """Fused halo exchange over peer memory (C ABI fse_ipc_* / fse_shard_set_peers):
+    this rank's frame and a pair of device flags are exported through CUDA IPC,
+    the neighbours' are mapped here, and a shard then runs all its levels in
+    one call -- the level kernel stores band-edge blocks straight into the
+    neighbour's frame and the streams order the levels through the flags (no
+    NCCL on the data path, no host round trip per level).  Construct once per
+    frame buffer on every rank (collective: all_gather of the handles)."""
+
+    def __init__(self, image_dev, rank: int, world: int, dist, group=None):
+        L = _lib.lib()
+        self.rank, self.world = rank, world
+        fl = ctypes.c_void_p()
+        _lib.check(L.fse_flags_alloc(ctypes.byref(fl)))
+        self.flags = fl
+        h_img = ctypes.create_string_buffer(_lib.FSE_IPC_HANDLE_BYTES)
+        h_flg = ctypes.create_string_buffer(_lib.FSE_IPC_HANDLE_BYTES)
+        _lib.check(L.fse_ipc_handle(ctypes.c_void_p(image_dev.data_ptr()), h_img))
+        _lib.check(L.fse_ipc_handle(fl, h_flg))
+        mine = (bytes(h_img.raw), bytes(h_flg.raw))
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        self._opened = []
+
+        def open_(h):
+            ptr = ctypes.c_void_p()
+            _lib.check(L.fse_ipc_open(ctypes.create_string_buffer(h, len(h)), ctypes.byref(ptr)))
+            self._opened.append(ptr)
+            return ptr
+
+        self.up = (open_(allh[rank - 1][0]), open_(allh[rank - 1][1])) if rank > 0 else (None, None)
+        self.down = (open_(allh[rank + 1][0]), open_(allh[rank + 1][1])) if rank < world - 1 else (None, None)
+        self.epoch = 1  # flags start at 0, epochs at 1
+
+    def attach(self, executor) -> None:
+        """Route this shard's halos through peer memory for its next run."""
+        _lib.check(_lib.lib().fse_shard_set_peers(executor.handle, self.up[0], self.up[1], self.down[0],
+                                                  self.down[1], self.flags, self.epoch))
+        self.epoch += 1
+
+    def close(self) -> None:
+        L = _lib.lib()
+        for p in self._opened:
+            L.fse_ipc_close(p)
+        self._opened = []
+        if self.flags is not None:
+            L.fse_flags_free(self.flags)
+            self.flags = None
+
+
+def run_levels_p2p(executor, link: PeerLink) -> None:
+    """The whole level sequence of one shard with the fused exchange."""
+    link.attach(executor)
+    _lib.check(_lib.lib().fse_shard_run(executor.handle, 0, executor.n_levels, executor.stream))
+
+
 def conceal_strips(image, mask, params: FseParams, precision: str = "fp32", order: str = "optimized",
-                   group=None, gather: bool = True):
+                   group=None, gather: bool = True, transport: str = "p2p"):
     """Conceal one frame on all ranks of the default process group (one GPU per
     rank).  Returns (image, mask) numpy arrays on rank 0 when gather=True (other
-    ranks get None), else this rank's band rows and its band."""
+    ranks get None), else this rank's band rows and its band.  transport "p2p"
+    = fused halo exchange over peer memory (PeerLink), "collective" = per-level
+    send/recv over torch.distributed (NCCL on GPUs)."""
+    if transport not in ("p2p", "collective"):
+        raise ValueError("transport must be 'p2p' or 'collective'")
     import torch
     import torch.distributed as dist
 
@@ -175,27 +238,44 @@ def conceal_strips(image, mask, params: FseParams, precision: str = "fp32", orde
     msk_d = torch.from_numpy(mask).cuda()
     out_d = torch.empty_like(msk_d)
     ex = ShardExecutor(plan, bands[rank], img_d, msk_d, out_d, params, precision)
-    flags_all = [ex.flags]
-    if world > 1:
-        t = torch.as_tensor(ex.flags, dtype=torch.int32, device="cuda")
-        gathered = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(gathered, t, group=group)
-        flags_all = [g.cpu().numpy() for g in gathered]
-    run_levels(ex, img_d, rank, world, bands, flags_all, ex.n_levels, R, B, H, dist, group)
-    ex.close()
+    if world > 1 and transport == "p2p":
+        link = PeerLink(img_d, rank, world, dist, group)
+        try:
+            run_levels_p2p(ex, link)
+            ex.close()
+            torch.cuda.synchronize()
+            dist.barrier(group=group)  # every rank's peer stores have landed
+        finally:
+            link.close()
+    else:
+        flags_all = [ex.flags]
+        if world > 1:
+            dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+            t = torch.as_tensor(ex.flags, dtype=torch.int32, device=dev)
+            gathered = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(gathered, t, group=group)
+            flags_all = [g.cpu().numpy() for g in gathered]
+        run_levels(ex, img_d, rank, world, bands, flags_all, ex.n_levels, R, B, H, dist, group)
+        ex.close()
     lo, hi = bands[rank]
     y0, y1 = lo * B, min(H, hi * B)
     if not gather:
         return img_d[y0:y1].double().cpu().numpy(), out_d[y0:y1].cpu().numpy(), bands[rank]
     if world > 1:
+        host = dist.get_backend(group) == "gloo"  # gloo moves host memory only
         if rank == 0:
             for r in range(1, world):
                 a, b = bands[r][0] * B, min(H, bands[r][1] * B)
-                dist.recv(img_d[a:b], r, group)
-                dist.recv(out_d[a:b], r, group)
+                for t in (img_d[a:b], out_d[a:b]):
+                    if host:
+                        hb = t.cpu()
+                        dist.recv(hb, r, group)
+                        t.copy_(hb)
+                    else:
+                        dist.recv(t, r, group)
         else:
-            dist.send(img_d[y0:y1].contiguous(), 0, group)
-            dist.send(out_d[y0:y1].contiguous(), 0, group)
+            for t in (img_d[y0:y1].contiguous(), out_d[y0:y1].contiguous()):
+                dist.send(t.cpu() if host else t, 0, group)
     if rank != 0:
         return None
     return img_d.double().cpu().numpy(), out_d.cpu().numpy()

@@ -2,6 +2,8 @@
 fse_conceal_frames) against the reference's golden outputs, plus the
 reference's pipeline properties (test_conceal.py, test_acceptance.py)."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -529,3 +531,19 @@ def test_tracked_and_lazy_argmax_identical(cfg, B, F):
         L.fse_set_track_below(148 * 16)
     assert outs[0] == outs[1]
     assert L.fse_set_track_below(-1) != 0
+
+
+@pytest.mark.parametrize("world,B", [(2, 4), (3, 2)])
+def test_strips_fused_peer_exchange_multi_process(world, B):
+    """Strip sharding over `world` processes (one GPU here; CUDA IPC maps the
+    neighbours' frames and flags): the fused halo exchange (peer stores in the
+    level kernel, device-flag ordering, one shard call per frame) and the
+    per-level collective exchange both reproduce the whole-frame conceal bit
+    for bit, twice in a row (flag epochs)."""
+    import subprocess
+    import sys
+
+    drv = os.path.join(os.path.dirname(os.path.abspath(__file__)), "strips_p2p_driver.py")
+    r = subprocess.run([sys.executable, drv, str(world), "5", str(B)], capture_output=True, text=True,
+                       timeout=400)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
