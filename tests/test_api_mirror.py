@@ -246,3 +246,13 @@ def test_conceal_argument_errors_without_device_work():  # conceal.py:113-120
         P.conceal(img, msk, order="linescan", threads=2)
     with pytest.raises(ValueError):
         P.conceal(img, np.zeros((8, 16), dtype=np.uint8))
+
+
+def test_stream_needs_a_device():
+    """No CPU fallback: the streaming API refuses to run without CUDA."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    with pytest.raises(RuntimeError):
+        P.ConcealStream(P.FseParams(), (16, 16))

@@ -547,3 +547,26 @@ def test_strips_fused_peer_exchange_multi_process(world, B):
     r = subprocess.run([sys.executable, drv, str(world), "5", str(B)], capture_output=True, text=True,
                        timeout=400)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("prec,batch,depth", [("fp32", 3, 2), ("fp64", 4, 3)])
+def test_conceal_stream_equals_per_frame(prec, batch, depth):
+    """ConcealStream (frames pushed one at a time, batched, upload / plan /
+    levels / download of neighbouring batches overlapped) returns, in push
+    order, exactly what conceal() gives per frame -- including a partial last
+    batch and more batches than slots (backpressure)."""
+    nf = 9
+    frames = [synth.synthetic_frame(96, 160, 70 + f, 6, 3) for f in range(nf)]
+    masks = [synth.loss_mask(96, 160, "mixed", 0.25, 80 + f) for f in range(nf)]
+    p = P.FseParams(d=14, iterations=30, block_size=4, fft_size=64)
+    got = []
+    with P.ConcealStream(p, (96, 160), batch=batch, precision=prec, depth=depth,
+                         in_dtype=np.float64 if prec == "fp64" else np.uint8) as st:
+        for f in range(nf):
+            got += st.push(frames[f], masks[f])
+        got += st.flush()
+    assert len(got) == nf
+    for f in range(nf):
+        one, om, _ = P.conceal(frames[f], masks[f], p, precision=prec)
+        assert got[f][0].astype(np.float64).tobytes() == one.tobytes()
+        np.testing.assert_array_equal(got[f][1], om)
