@@ -16,10 +16,18 @@ namespace fse {
 // halves the fp32 occupancy)
 template <typename T> using Fast64 = FastCfg<T, 64, 6, sizeof(T) == 4, sizeof(T) == 4 ? 4 : 3>;  // fp64: plain W plane
 
-template <typename T> using Fast32 = FastCfg<T, 32, 6>;
+// F = 32 fp32: 3 warps per window (6 bins per thread), 8 CTAs per SM --
+// config 5 B=2 (1.04M windows of 30x30): 95 ms vs 120 ms with 6 warps
+// (measured NW/MINB: 6/0 120, 3/10 98, 3/6 104, 2/12 99, 2/16 109, 1/16 115 ms)
+#ifndef FSE_F32_32_NW  // dev knob
+#define FSE_F32_32_NW 3
+#define FSE_F32_32_MINB 8
+#endif
+template <typename T>
+using Fast32 = FastCfg<T, 32, sizeof(T) == 4 ? FSE_F32_32_NW : 6, true, sizeof(T) == 4 ? FSE_F32_32_MINB : 0>;
 // tracked-argmax fp32 twins for narrow levels (see FastCfg::TRACK)
 using Fast64T = FastCfg<float, 64, 6, true, 4, 1, true>;
-using Fast32T = FastCfg<float, 32, 6, true, 0, 1, true>;
+using Fast32T = FastCfg<float, 32, FSE_F32_32_NW, true, FSE_F32_32_MINB, 1, true>;
 
 // Levels narrower than this many windows use the tracked argmax (fp32):
 // measured on configs 2 (linescan), 3 and 5 -- levels of a few hundred
@@ -40,7 +48,10 @@ static int track_below(int sms) {
 }
 // F = 128 (fp32 only: the row-extended W plane is 193 x 128 x 8 B = 198 KB):
 // 260 row segments over 20 warps -> 13 bins per thread, one CTA per SM.
-template <typename T> using Fast128 = FastCfg<T, 128, 20>;
+#ifndef FSE_F128_NW  // dev knob: warps per window of the fp32 F = 128 kernel
+#define FSE_F128_NW 20
+#endif
+template <typename T> using Fast128 = FastCfg<T, 128, FSE_F128_NW>;
 // Cluster variants for levels narrower than the GPU: one window over CL SMs.
 template <typename T, int CL> using Fast64C = FastCfg<T, 64, 6, sizeof(T) == 4, 0, CL>;
 template <typename T, int CL> using Fast32C = FastCfg<T, 32, 6, true, 0, CL>;
