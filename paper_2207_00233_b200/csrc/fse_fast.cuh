@@ -68,6 +68,10 @@ struct FastCfg {
     static constexpr int NB = (NSEGS + NWT - 1) / NWT;  // segments (bins) per thread
     static constexpr int RSTEP = NWT / SEG;     // row stride between a warp's segments
     static constexpr int EXT_ROWS = 3 * F_ / 2 + 1;
+    // threads summing the block model (see the write-back): the smallest
+    // CTA of any variant of this F
+    static constexpr int NSUB_BASE = F_ == 32 ? 96 : F_ == 64 ? 192 : 640;
+    static_assert(NW_ * 32 >= NSUB_BASE, "model subsets need NSUB_BASE threads");
     static_assert(F_ == 32 || F_ == 64 || F_ == 128, "fast path: F = 32, 64 or 128");
     static_assert(NW_ % SEG == 0, "NW must be a multiple of F/32");
     static_assert(NWT <= 32, "one warp reduces the window's slots");
@@ -947,8 +951,11 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
             }
         };
         if (crank == 0) {  // the cluster's CTA 0 writes the block
-            if (nsamp <= NT) {
-                const int nsub = NT / nsamp, q = t % nsamp, r = t / nsamp;
+            // the subset count depends on F and the block only (not on the
+            // warps of this variant), so every variant of one F sums the model
+            // in the same order and gives bit-identical samples
+            if (nsamp <= C::NSUB_BASE) {
+                const int nsub = C::NSUB_BASE / nsamp, q = t % nsamp, r = t / nsamp;
                 T *red2 = reinterpret_cast<T *>(big);
                 if (r < nsub) red2[r * nsamp + q] = model(q, r, nsub);
                 __syncthreads();

@@ -27,6 +27,11 @@ template <typename T>
 using Fast32 = FastCfg<T, 32, sizeof(T) == 4 ? FSE_F32_32_NW : 6, true, sizeof(T) == 4 ? FSE_F32_32_MINB : 0>;
 // tracked-argmax fp32 twins for narrow levels (see FastCfg::TRACK)
 using Fast64T = FastCfg<float, 64, 6, true, 4, 1, true>;
+// levels of at most one window per SM (config 2; config 5 bands at N = 8):
+// 12 warps per window (6 bins per thread) shorten a lone window's iteration --
+// config 2 5.3 -> 5.0 ms; with more windows per level the 6-warp form wins
+// (config 3: 19.8 vs 23.3 ms; 22 warps: slower everywhere)
+using Fast64L = FastCfg<float, 64, 12, true, 2, 1, true>;
 using Fast32T = FastCfg<float, 32, FSE_F32_32_NW, true, FSE_F32_32_MINB, 1, true>;
 
 // Levels narrower than this many windows use the tracked argmax (fp32):
@@ -216,6 +221,8 @@ int fast_level(int dtype, int F, bool guard, const FastArgs &a, int grid, int Mm
         const bool narrow = grid < track_below(sms);
         if (F == 64) {
             if (guard) return launch<Fast64<float>, 0, true>(a, grid, Mmax, Nmax, model_n, s);
+            if (narrow && grid <= sms && track_below(sms) > 0)
+                return launch<Fast64L, 0, false>(a, grid, Mmax, Nmax, model_n, s);
             return narrow ? launch<Fast64T, 0, false>(a, grid, Mmax, Nmax, model_n, s)
                           : launch<Fast64<float>, 0, false>(a, grid, Mmax, Nmax, model_n, s);
         }
