@@ -58,20 +58,30 @@ int validate(const FseParamsC *p, int32_t H, int32_t W, int32_t order) {
 
 // schedule.py:28-57 on a row-major lossy table
 void init_counts_impl(const uint8_t *lossy, int rows, int cols, int32_t *counts) {
+    // 3x3 box sums of the lossy map through a zero-padded copy (no bounds
+    // tests in the inner loop), minus the block itself
+    const int pc = cols + 2;
+    std::vector<uint8_t> pad((size_t)(rows + 2) * pc, 0);
     for (int r = 0; r < rows; ++r)
+        for (int c = 0; c < cols; ++c) pad[(size_t)(r + 1) * pc + c + 1] = lossy[(size_t)r * cols + c] ? 1 : 0;
+    std::vector<uint8_t> h3((size_t)(rows + 2) * cols);  // horizontal 3-sums of each padded row
+    for (int r = 0; r < rows + 2; ++r) {
+        const uint8_t *p = &pad[(size_t)r * pc];
+        uint8_t *o = &h3[(size_t)r * cols];
+        for (int c = 0; c < cols; ++c) o[c] = (uint8_t)(p[c] + p[c + 1] + p[c + 2]);
+    }
+    for (int r = 0; r < rows; ++r) {
+        const uint8_t *a = &h3[(size_t)r * cols], *m = &h3[(size_t)(r + 1) * cols], *z = &h3[(size_t)(r + 2) * cols];
+        const int er = (r == 0) + (r == rows - 1);
         for (int c = 0; c < cols; ++c) {
-            int32_t n = 0;
-            for (int dr = -1; dr <= 1; ++dr)
-                for (int dc = -1; dc <= 1; ++dc) {
-                    if (!dr && !dc) continue;
-                    int rr = r + dr, cc = c + dc;
-                    if (rr >= 0 && rr < rows && cc >= 0 && cc < cols && lossy[rr * cols + cc]) ++n;
-                }
-            int edges = (r == 0) + (r == rows - 1) + (c == 0) + (c == cols - 1);
+            const int self = lossy[(size_t)r * cols + c] ? 1 : 0;
+            int n = a[c] + m[c] + z[c] - self;
+            const int edges = er + (c == 0) + (c == cols - 1);
             if (edges == 1) n += kMarginBonus;
             else if (edges >= 2) n += kCornerBonus;
-            counts[r * cols + c] = lossy[r * cols + c] ? n : -1;
+            counts[(size_t)r * cols + c] = self ? n : -1;
         }
+    }
 }
 
 // schedule.py:60-105 with a bucket queue: one bitset of pending blocks per
@@ -81,7 +91,10 @@ void schedule_impl(const int32_t *counts_in, int rows, int cols,
                    std::vector<int32_t> &ptr, std::vector<int32_t> &blocks) {
     const int nb = rows * cols;
     const int words = (nb + 63) / 64;
-    std::vector<int32_t> cnt(counts_in, counts_in + nb);
+    // counts fit in int8: at most 8 + 5 at the start, done blocks drift down
+    // to -1 - 8 (schedule.py:85-94); one byte per block keeps them in cache
+    std::vector<int8_t> cnt(nb);
+    for (int b = 0; b < nb; ++b) cnt[b] = (int8_t)std::max(-128, std::min(127, (int)counts_in[b]));
     int maxc = 0;
     long pending = 0;
     for (int b = 0; b < nb; ++b)
@@ -89,62 +102,57 @@ void schedule_impl(const int32_t *counts_in, int rows, int cols,
             maxc = std::max(maxc, (int)cnt[b]);
             ++pending;
         }
-    // bucket[c]: bitset of pending blocks with count c; summ[c]: bitset of its
-    // non-zero words, so a row-major scan skips empty stretches 64 words at a time
+    // bucket c: bitset of pending blocks with count c; summary: bitset of its
+    // non-zero words, so a row-major scan skips empty stretches 64 words at a
+    // time.  The count is the fast index of both arrays: a neighbour's move
+    // from bucket c to c - 1 touches one cache line, not two far-apart ones.
+    const int NC = maxc + 1;
     const int swords = (words + 63) / 64;
-    std::vector<std::vector<uint64_t>> bucket(maxc + 1, std::vector<uint64_t>(words, 0));
-    std::vector<std::vector<uint64_t>> summ(maxc + 1, std::vector<uint64_t>(swords, 0));
-    std::vector<long> bsize(maxc + 1, 0);
-    for (int b = 0; b < nb; ++b)
-        if (cnt[b] >= 0) {
-            bucket[cnt[b]][b >> 6] |= 1ull << (b & 63);
-            summ[cnt[b]][b >> 12] |= 1ull << ((b >> 6) & 63);
-            ++bsize[cnt[b]];
-        }
+    std::vector<uint64_t> bits((size_t)words * NC, 0), summ((size_t)swords * NC, 0);
+    std::vector<long> bsize(NC, 0);
     auto add = [&](int c, int b) {
-        bucket[c][b >> 6] |= 1ull << (b & 63);
-        summ[c][b >> 12] |= 1ull << ((b >> 6) & 63);
+        bits[(size_t)(b >> 6) * NC + c] |= 1ull << (b & 63);
+        summ[(size_t)(b >> 12) * NC + c] |= 1ull << ((b >> 6) & 63);
         ++bsize[c];
     };
     auto del = [&](int c, int b) {
-        uint64_t &w = bucket[c][b >> 6];
+        uint64_t &w = bits[(size_t)(b >> 6) * NC + c];
         w &= ~(1ull << (b & 63));
-        if (!w) summ[c][b >> 12] &= ~(1ull << ((b >> 6) & 63));
+        if (!w) summ[(size_t)(b >> 12) * NC + c] &= ~(1ull << ((b >> 6) & 63));
         --bsize[c];
     };
-    std::vector<int32_t> taken(nb, -1);
+    for (int b = 0; b < nb; ++b)
+        if (cnt[b] >= 0) add(cnt[b], b);
+    // blocks taken in the current phase (reset through the batch list)
+    std::vector<uint8_t> taken(nb, 0);
     ptr.assign(1, 0);
     blocks.clear();
     blocks.reserve(pending);
     std::vector<int32_t> batch;
-    int phase = 0;
     while (pending > 0) {
         int nmin = 0;
         while (bsize[nmin] == 0) ++nmin;
         batch.clear();
-        auto &bits = bucket[nmin];
-        auto &sum = summ[nmin];
         for (int sw = 0; sw < swords; ++sw) {
-            uint64_t sm = sum[sw];
+            uint64_t sm = summ[(size_t)sw * NC + nmin];
             while (sm) {
                 const int w = (sw << 6) + __builtin_ctzll(sm);
                 sm &= sm - 1;
-                uint64_t m = bits[w];
+                uint64_t m = bits[(size_t)w * NC + nmin];
                 while (m) {
                     int b = (w << 6) + __builtin_ctzll(m);
                     m &= m - 1;
                     int r = b / cols, c = b - r * cols;
                     // only row-major-earlier neighbours can already be taken
                     bool clash = false;
-                    if (c > 0 && taken[b - 1] == phase) clash = true;
+                    if (c > 0 && taken[b - 1]) clash = true;
                     if (!clash && r > 0) {
                         int up = b - cols;
-                        if (taken[up] == phase || (c > 0 && taken[up - 1] == phase) ||
-                            (c + 1 < cols && taken[up + 1] == phase))
+                        if (taken[up] || (c > 0 && taken[up - 1]) || (c + 1 < cols && taken[up + 1]))
                             clash = true;
                     }
                     if (clash) continue;
-                    taken[b] = phase;
+                    taken[b] = 1;
                     batch.push_back(b);
                 }
             }
@@ -152,6 +160,7 @@ void schedule_impl(const int32_t *counts_in, int rows, int cols,
         for (int b : batch) {
             del(nmin, b);
             cnt[b] = -1;
+            taken[b] = 0;
             --pending;
         }
         for (int b : batch) {
@@ -173,7 +182,6 @@ void schedule_impl(const int32_t *counts_in, int rows, int cols,
         }
         blocks.insert(blocks.end(), batch.begin(), batch.end());
         ptr.push_back((int32_t)blocks.size());
-        ++phase;
     }
 }
 
@@ -194,6 +202,42 @@ struct Geometry {
         c1 = std::min(W, c1 + d);
     }
 };
+
+// Dependency levels over the processing order: level(b) = 1 + max level over
+// lower-rank blocks whose samples b's window covers.  The window of block
+// (r, c) covers exactly the blocks within Chebyshev radius R = ceil(d / B)
+// (clamped to the grid): its rows run from floor((rB - d)/B) = r - ceil(d/B)
+// to floor((rB + B + d - 1)/B) = r + ceil(d/B).  The square max is separable:
+// HL[r][c] = max of level over row r, columns c +- R, kept up to date as
+// batches are committed; a query is 2R+1 reads of HL.  T = int16_t while the
+// level count fits (half the cache footprint of int32).
+template <typename T>
+int level_pass(const Plan &P, int rows, int cols, int R, std::vector<int32_t> &level) {
+    std::vector<T> HL((size_t)rows * cols, (T)-1);
+    int n_levels = 0;
+    const int n_batches = (int)P.batch_ptr.size() - 1;
+    for (int k = 0; k < n_batches; ++k) {
+        const int i0 = P.batch_ptr[k], i1 = P.batch_ptr[k + 1];
+        for (int i = i0; i < i1; ++i) {  // a batch reads only earlier batches
+            const int b = P.batch_blocks[i];
+            const int r = b / cols, c = b - r * cols;
+            int m = -1;
+            for (int rr = std::max(0, r - R); rr <= std::min(rows - 1, r + R); ++rr)
+                m = std::max(m, (int)HL[(size_t)rr * cols + c]);
+            level[b] = m + 1;
+            n_levels = std::max(n_levels, m + 2);
+        }
+        for (int i = i0; i < i1; ++i) {
+            const int b = P.batch_blocks[i];
+            const int r = b / cols, c = b - r * cols;
+            T *row = &HL[(size_t)r * cols];
+            const T lv = (T)level[b];
+            for (int cc = std::max(0, c - R); cc <= std::min(cols - 1, c + R); ++cc)
+                row[cc] = std::max(row[cc], lv);
+        }
+    }
+    return n_levels;
+}
 
 int build_one(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p, int32_t order,
               Plan &P) {
@@ -297,8 +341,13 @@ int build_one(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p, in
         return PS[(ihi + 1) * C1 + jhi + 1] - PS[ilo * C1 + jhi + 1] - PS[(ihi + 1) * C1 + jlo] +
                    PS[ilo * C1 + jlo] > 0;
     };
+    // the static test for every lossy block in one row-major pass (the prefix
+    // sums are then read in address order instead of in phase order)
+    std::vector<uint8_t> sok(nb, 0);
+    for (int b = 0; b < nb; ++b)
+        if (lossy[b]) sok[b] = static_usable(b) ? 1 : 0;
     auto usable = [&](int b) -> bool {
-        if (static_usable(b)) return true;
+        if (sok[b]) return true;
         int wr0, wr1, wc0, wc1;
         G.window_rect(b, wr0, wr1, wc0, wc1);
         int br0 = wr0 / B, br1 = (wr1 - 1) / B, bc0 = wc0 / B, bc1 = (wc1 - 1) / B;
@@ -374,37 +423,12 @@ int build_one(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p, in
     P.n_processed = (int32_t)P.batch_blocks.size();
 
     lap("ranks");
-    // dependency levels over the processing order
+    // dependency levels over the processing order (level_pass)
     std::vector<int32_t> level(nb, -1);
-    // The window of block (r, c) covers exactly the blocks within Chebyshev
-    // radius R = ceil(d / B) (clamped to the grid): its rows run from
-    // floor((rB - d)/B) = r - ceil(d/B) to floor((rB + B + d - 1)/B) = r + ceil(d/B).
-    // level(b) = 1 + max level over lower-rank blocks in that square.  The square
-    // max is separable: HL[r][c] = max of level over row r, columns c +- R, kept
-    // up to date as batches are committed; a query is R*2+1 reads of HL.
     const int R = (p->d + B - 1) / B;
-    std::vector<int32_t> HL(nb, -1);
-    int n_levels = 0;
     const int n_batches = (int)P.batch_ptr.size() - 1;
-    for (int k = 0; k < n_batches; ++k) {
-        const int i0 = P.batch_ptr[k], i1 = P.batch_ptr[k + 1];
-        for (int i = i0; i < i1; ++i) {  // a batch reads only earlier batches
-            const int b = P.batch_blocks[i];
-            const int r = b / cols, c = b - r * cols;
-            int m = -1;
-            for (int rr = std::max(0, r - R); rr <= std::min(rows - 1, r + R); ++rr)
-                m = std::max(m, HL[rr * cols + c]);
-            level[b] = m + 1;
-            n_levels = std::max(n_levels, m + 2);
-        }
-        for (int i = i0; i < i1; ++i) {
-            const int b = P.batch_blocks[i];
-            const int r = b / cols, c = b - r * cols;
-            int32_t *row = &HL[r * cols];
-            for (int cc = std::max(0, c - R); cc <= std::min(cols - 1, c + R); ++cc)
-                row[cc] = std::max(row[cc], level[b]);
-        }
-    }
+    int n_levels = n_batches < 32000 ? level_pass<int16_t>(P, rows, cols, R, level)
+                                     : level_pass<int32_t>(P, rows, cols, R, level);
     P.level_ptr.assign(n_levels + 1, 0);
     for (int b : P.batch_blocks) ++P.level_ptr[level[b] + 1];
     for (int l = 0; l < n_levels; ++l) P.level_ptr[l + 1] += P.level_ptr[l];
