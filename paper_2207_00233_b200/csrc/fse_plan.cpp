@@ -163,21 +163,29 @@ void schedule_impl(const int32_t *counts_in, int rows, int cols,
             taken[b] = 0;
             --pending;
         }
+        auto release = [&](int o) {
+            if (cnt[o] >= 0) {
+                del(cnt[o], o);
+                --cnt[o];
+                add(cnt[o], o);
+            } else {
+                --cnt[o];  // done blocks drift below -1 (schedule.py:85-94)
+            }
+        };
         for (int b : batch) {
             int r = b / cols, c = b - r * cols;
+            if (r > 0 && r + 1 < rows && c > 0 && c + 1 < cols) {  // interior: no bounds tests
+                const int u = b - cols, d = b + cols;
+                release(u - 1), release(u), release(u + 1), release(b - 1);
+                release(b + 1), release(d - 1), release(d), release(d + 1);
+                continue;
+            }
             for (int dr = -1; dr <= 1; ++dr)
                 for (int dc = -1; dc <= 1; ++dc) {
                     if (!dr && !dc) continue;
                     int rr = r + dr, cc = c + dc;
                     if (rr < 0 || rr >= rows || cc < 0 || cc >= cols) continue;
-                    int o = rr * cols + cc;
-                    if (cnt[o] >= 0) {
-                        del(cnt[o], o);
-                        --cnt[o];
-                        add(cnt[o], o);
-                    } else {
-                        --cnt[o];  // done blocks drift below -1 (schedule.py:85-94)
-                    }
+                    release(rr * cols + cc);
                 }
         }
         blocks.insert(blocks.end(), batch.begin(), batch.end());
@@ -321,31 +329,47 @@ int build_one(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p, in
     const bool r_counts = p->delta > 0.0;
     // Fast path: a block lying wholly inside the window that holds an A sample
     // (or, with delta > 0, a pre-reconstructed sample) makes the window usable
-    // whatever was written since; count such blocks with a 2-D prefix sum.
-    std::vector<int32_t> PS((size_t)(rows + 1) * (cols + 1), 0);
-    for (int r = 0; r < rows; ++r)
-        for (int c = 0; c < cols; ++c) {
-            const int o = r * cols + c;
-            const int ok = nA(o) || (r_counts && nR0(o));
-            PS[(size_t)(r + 1) * (cols + 1) + c + 1] = ok + PS[(size_t)r * (cols + 1) + c + 1] +
-                                                       PS[(size_t)(r + 1) * (cols + 1) + c] -
-                                                       PS[(size_t)r * (cols + 1) + c];
-        }
-    auto static_usable = [&](int b) -> bool {
-        int wr0, wr1, wc0, wc1;
-        G.window_rect(b, wr0, wr1, wc0, wc1);
-        const int ilo = (wr0 + B - 1) / B, ihi = wr1 == H ? rows - 1 : wr1 / B - 1;
-        const int jlo = (wc0 + B - 1) / B, jhi = wc1 == W ? cols - 1 : wc1 / B - 1;
-        if (ilo > ihi || jlo > jhi) return false;
-        const size_t C1 = cols + 1;
-        return PS[(ihi + 1) * C1 + jhi + 1] - PS[ilo * C1 + jhi + 1] - PS[(ihi + 1) * C1 + jlo] +
-                   PS[ilo * C1 + jlo] > 0;
-    };
-    // the static test for every lossy block in one row-major pass (the prefix
-    // sums are then read in address order instead of in phase order)
+    // whatever was written since.  The fully covered block range of block
+    // (r, c)'s window is [ilo(r), ihi(r)] x [jlo(c), jhi(c)], both monotone in
+    // their argument, so one row-major sweep with vertical running counts per
+    // column and a prefix count along the row answers every block in O(1).
     std::vector<uint8_t> sok(nb, 0);
-    for (int b = 0; b < nb; ++b)
-        if (lossy[b]) sok[b] = static_usable(b) ? 1 : 0;
+    {
+        auto lo_hi = [&](int i, int n, int S, int &lo, int &hi) {  // block i of n along an axis of S samples
+            const int s0 = std::max(0, i * B - p->d);
+            const int s1 = std::min(S, std::min(i * B + B, S) + p->d);
+            lo = (s0 + B - 1) / B;
+            hi = s1 == S ? n - 1 : s1 / B - 1;
+        };
+        std::vector<int> jlo(cols), jhi(cols);
+        for (int c = 0; c < cols; ++c) lo_hi(c, cols, W, jlo[c], jhi[c]);
+        std::vector<int32_t> vcnt(cols, 0), pre(cols + 1, 0);
+        int cur_lo = 0, cur_hi = -1;  // block rows summed into vcnt
+        for (int r = 0; r < rows; ++r) {
+            int ilo, ihi;
+            lo_hi(r, rows, H, ilo, ihi);
+            if (ilo > ihi) continue;
+            while (cur_hi < ihi) {
+                ++cur_hi;
+                for (int c = 0; c < cols; ++c) {
+                    const int o = cur_hi * cols + c;
+                    vcnt[c] += (nA(o) || (r_counts && nR0(o))) ? 1 : 0;
+                }
+            }
+            while (cur_lo < ilo) {
+                for (int c = 0; c < cols; ++c) {
+                    const int o = cur_lo * cols + c;
+                    vcnt[c] -= (nA(o) || (r_counts && nR0(o))) ? 1 : 0;
+                }
+                ++cur_lo;
+            }
+            for (int c = 0; c < cols; ++c) pre[c + 1] = pre[c] + (vcnt[c] > 0 ? 1 : 0);
+            for (int c = 0; c < cols; ++c) {
+                const int b = r * cols + c;
+                if (lossy[b] && jlo[c] <= jhi[c]) sok[b] = pre[jhi[c] + 1] - pre[jlo[c]] > 0 ? 1 : 0;
+            }
+        }
+    }
     auto usable = [&](int b) -> bool {
         if (sok[b]) return true;
         int wr0, wr1, wc0, wc1;
