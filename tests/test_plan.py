@@ -13,6 +13,7 @@ from hypothesis import strategies as st
 
 import paper_2207_00233_b200 as P
 from helpers import conceal_case, csr, emulate_levels
+from oracle import oracle as O
 from paper_2207_00233_b200 import _lib
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -198,3 +199,88 @@ def test_plan_many_threads_equals_single():
         one = P.build_plan(m, p)
         assert pl.batches() == one.batches() and pl.levels() == one.levels()
         np.testing.assert_array_equal(pl.ranks(), one.ranks())
+
+
+def _reference_order(mask, B, d, delta, order):
+    """The reference's processing order restated in Python (schedule.py:28-105
+    phases or the linescan sequence, conceal.py:145-163 snapshot batches with
+    the degeneracy test of fse.py:150-151, conceal.py:69-94 retry sweeps):
+    returns (batches, unconcealed)."""
+    H, W = mask.shape
+    g = O.Grid.of(H, W, B)
+    lossy = O.lost_per_block(g, mask).reshape(-1) > 0
+    if order == "optimized":
+        phases = O.schedule_all(g, O.init_counts(g, lossy.reshape(g.rows, g.cols)))
+    else:
+        phases = [[b] for b in np.flatnonzero(lossy).tolist()]
+    state = mask.copy()
+
+    def usable(b):
+        _, cls, _ = O.classify(g, state, b, d)
+        return (O.weight_plane(cls.shape, cls, 0.8, delta) > 0).any()
+
+    def write(b):
+        r0, r1, c0, c1 = g.bounds(b)
+        sub = state[r0:r1, c0:c1]
+        sub[sub == O.LOST] = O.RECONSTRUCTED
+
+    batches, deferred = [], []
+    for ph in phases:
+        ok = [b for b in ph if usable(b)]
+        deferred += [b for b in ph if b not in ok]
+        for b in ok:  # snapshot: writes land after the whole batch
+            write(b)
+        if ok:
+            batches.append(ok)
+    pending = sorted(deferred)
+    for _ in range(max(g.rows, g.cols)):
+        if not pending:
+            break
+        still = []
+        for b in pending:
+            if usable(b):
+                write(b)
+                batches.append([b])
+            else:
+                still.append(b)
+        if len(still) == len(pending):
+            break
+        pending = still
+    return batches, pending
+
+
+def test_plan_matches_python_restatement_on_random_masks():
+    """build_plan (C++: bucket-queue scheduler, static/dynamic usability,
+    retry sweeps, dependency levels) against the Python restatement of the
+    reference's order on random masks: ragged grids, RECONSTRUCTED samples,
+    delta = 0 (R samples weightless), fully lost frames, both orders.  Levels
+    must order every pair of overlapping blocks like their ranks."""
+    rng = np.random.default_rng(17)
+    for t in range(120):
+        H, W = int(rng.integers(1, 48)), int(rng.integers(1, 48))
+        B, d = int(rng.integers(1, 7)), int(rng.integers(0, 12))
+        delta = float(rng.choice([0.0, 0.2]))
+        order = str(rng.choice(["optimized", "linescan"]))
+        mask = rng.choice(np.array([0, 1, 2], dtype=np.uint8), size=(H, W), p=rng.dirichlet([1, 1, 0.3]))
+        if t % 10 == 0:
+            mask[:] = 1
+        mask = np.ascontiguousarray(mask)
+        p = P.FseParams(d=d, delta=delta, iterations=5, block_size=B)
+        plan = P.build_plan(mask, p, order)
+        batches, unconcealed = _reference_order(mask, B, d, delta, order)
+        assert plan.batches() == batches, (t, H, W, B, d, delta, order)
+        assert plan.unconcealed() == unconcealed
+        # levels: a block's level exceeds that of every lower-rank block its window covers
+        rk = plan.ranks()
+        lv = np.full(rk.shape, -1)
+        for l, blocks in enumerate(plan.levels()):
+            lv[blocks] = l
+        R = -(-d // B) if d > 0 else 0
+        cols = plan.cols
+        for b in np.flatnonzero(lv >= 0):
+            r, c = divmod(int(b), cols)
+            for rr in range(max(0, r - R), min(plan.rows, r + R + 1)):
+                for cc in range(max(0, c - R), min(cols, c + R + 1)):
+                    o = rr * cols + cc
+                    if lv[o] >= 0 and rk[o] < rk[b]:
+                        assert lv[o] < lv[b]
