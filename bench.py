@@ -67,8 +67,8 @@ def args_():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-second", action="store_true", help="skip the other precision's measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-blocks", type=int, default=2000,
-                    help="cpu_baseline sample: lossy blocks of frame 0 (about 10 s single core)")
+    ap.add_argument("--cpu-blocks", type=int, default=5200,
+                    help="cpu_baseline sample: lossy blocks of frame 0 (about 10 s on one core of the GPU box)")
     return ap.parse_args()
 
 
