@@ -875,8 +875,16 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         blin = 0xFFFFFFFFu;
         tmax = (T)0;
         const T2 mS = T2{-gpr, -gpr}, qv = T2{gpi, -gpi};
-        // loads of a group of LG bins are issued before its math (smem latency)
-        constexpr int LG = IS_F32 ? 4 : 2;
+        // loads of a group of LG bins are issued before its math (smem latency);
+        // measured on config 4: fp32 LG 1/2/3/4/6/11 = 284.2/283.4/289.2/287.5/
+        // 292.5/302.4 ms, fp64 LG 1/2/3 = 554.4/558.8/554.9 ms
+#ifndef FSE_LG32
+#define FSE_LG32 2
+#endif
+#ifndef FSE_LG64
+#define FSE_LG64 1
+#endif
+        constexpr int LG = IS_F32 ? FSE_LG32 : FSE_LG64;
 #pragma unroll
         for (int j0 = 0; j0 < NB; j0 += LG) {
             T2 wl[LG], wh[LG];
