@@ -383,7 +383,16 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         const IT *img = reinterpret_cast<const IT *>(fd->image);
         const uint8_t *msk = fd->mask;
         const int32_t *rnk = fd->rank;
-        constexpr int RB = 4;
+        // staged window rows per warp pass (loads issued before their math);
+        // measured on config 4: fp32 RB 2/4/6 = 285.5/283.3/286.1 ms, fp64
+        // RB 4/6/8 = 554.4/548.5/558.4 ms
+#ifndef FSE_RB
+#define FSE_RB 4
+#endif
+#ifndef FSE_RB64
+#define FSE_RB64 6
+#endif
+        constexpr int RB = IS_F32 ? FSE_RB : FSE_RB64;
         for (int jc = 0; jc < N; jc += 32) {
             const int j = jc + lane;
             const bool jin = j < N;
@@ -519,7 +528,14 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     const int q4 = v / QW, v0 = v - q4 * QW;
     // the twiddle sequence e^{-j 2 pi v0 n / F}, n = q4 + 4 i, is the same for
     // every row: its first NR terms (n < 4 NR) stay in registers
-    constexpr int NR = IS_F32 ? 8 : 4;
+    // (measured: fp32 NR 4/6/8 = 293.9/293.3/283.3 ms; fp64 NR 4/6/8 = 554/571/583 ms, spills)
+#ifndef FSE_NR32
+#define FSE_NR32 8
+#endif
+#ifndef FSE_NR64
+#define FSE_NR64 4
+#endif
+    constexpr int NR = IS_F32 ? FSE_NR32 : FSE_NR64;
     const int tstep = (4 * v0) & (F - 1);
     T2 twr[NR];
 #pragma unroll
