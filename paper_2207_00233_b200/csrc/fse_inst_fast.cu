@@ -57,6 +57,10 @@ static int track_below(int sms) {
 #define FSE_F128_NW 20
 #endif
 template <typename T> using Fast128 = FastCfg<T, 128, FSE_F128_NW>;
+#ifndef FSE_F128T_NW
+#define FSE_F128T_NW FSE_F128_NW
+#endif
+using Fast128T = FastCfg<float, 128, FSE_F128T_NW, true, 0, 1, true>;
 // Cluster variants for levels narrower than the GPU: one window over CL SMs.
 template <typename T, int CL> using Fast64C = FastCfg<T, 64, 6, sizeof(T) == 4, 0, CL>;
 template <typename T, int CL> using Fast32C = FastCfg<T, 32, 6, true, 0, CL>;
@@ -217,8 +221,10 @@ int fast_level(int dtype, int F, bool guard, const FastArgs &a, int grid, int Mm
                     : launch_cluster<Fast32C<double, 2>>(a, grid, Mmax, Nmax, model_n, s);
     }
     if (dtype == FSE_F32) {
-        if (F == 128) return launch<Fast128<float>, 0, false>(a, grid, Mmax, Nmax, model_n, s);
         const bool narrow = grid < track_below(sms);
+        if (F == 128)
+            return narrow ? launch<Fast128T, 0, false>(a, grid, Mmax, Nmax, model_n, s)
+                          : launch<Fast128<float>, 0, false>(a, grid, Mmax, Nmax, model_n, s);
         if (F == 64) {
             if (guard) return launch<Fast64<float>, 0, true>(a, grid, Mmax, Nmax, model_n, s);
             if (narrow && grid <= sms && track_below(sms) > 0)
