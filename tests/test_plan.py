@@ -284,3 +284,20 @@ def test_plan_matches_python_restatement_on_random_masks():
                     o = rr * cols + cc
                     if lv[o] >= 0 and rk[o] < rk[b]:
                         assert lv[o] < lv[b]
+
+
+def test_abi_argument_errors_without_a_device():
+    """Entry points added for the fused halo exchange and the level-width
+    switch reject bad arguments with the ABI's error codes before touching
+    CUDA (no exception crosses the C boundary)."""
+    import ctypes
+
+    L = _lib.lib()
+    assert L.fse_shard_set_peers(None, None, None, None, None, None, 1) == _lib.FSE_EINVAL
+    assert L.fse_ipc_handle(None, None) == _lib.FSE_EINVAL
+    assert L.fse_ipc_open(None, None) == _lib.FSE_EINVAL
+    assert L.fse_ipc_close(ctypes.c_void_p(0x1234)) == _lib.FSE_EINVAL
+    assert L.fse_flags_alloc(None) == _lib.FSE_EINVAL
+    assert L.fse_set_track_below(-1) == _lib.FSE_EINVAL
+    assert b"track_below" in L.fse_last_error()
+    assert L.fse_shard_run(None, 0, 1, None) == _lib.FSE_EINVAL
