@@ -129,7 +129,12 @@ void schedule_impl(const int32_t *counts_in, int rows, int cols,
     blocks.clear();
     blocks.reserve(pending);
     std::vector<int32_t> batch;
+    const bool prof = getenv("FSE_PLAN_TIMING") != nullptr;
+    double t_sel = 0.0, t_com = 0.0;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
     while (pending > 0) {
+        const auto q0 = prof ? now() : std::chrono::steady_clock::time_point{};
         int nmin = 0;
         while (bsize[nmin] == 0) ++nmin;
         batch.clear();
@@ -157,6 +162,8 @@ void schedule_impl(const int32_t *counts_in, int rows, int cols,
                 }
             }
         }
+        const auto q1 = prof ? now() : std::chrono::steady_clock::time_point{};
+        if (prof) t_sel += ms(q0, q1);
         for (int b : batch) {
             del(nmin, b);
             cnt[b] = -1;
@@ -190,7 +197,9 @@ void schedule_impl(const int32_t *counts_in, int rows, int cols,
         }
         blocks.insert(blocks.end(), batch.begin(), batch.end());
         ptr.push_back((int32_t)blocks.size());
+        if (prof) t_com += ms(q1, now());
     }
+    if (prof) fprintf(stderr, "plan   schedule loop: select %.1f ms, commit %.1f ms\n", t_sel, t_com);
 }
 
 struct Geometry {
@@ -312,6 +321,7 @@ int build_one(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p, in
     if (order == FSE_ORDER_OPTIMIZED) {
         std::vector<int32_t> counts(nb);
         init_counts_impl(lossy.data(), rows, cols, counts.data());
+        lap("init_counts");
         schedule_impl(counts.data(), rows, cols, ph_ptr, ph_blocks);
     } else {
         ph_ptr.assign(1, 0);
