@@ -168,16 +168,25 @@ class PeerLink:
     def __init__(self, image_dev, rank: int, world: int, dist, group=None):
         L = _lib.lib()
         self.rank, self.world = rank, world
-        fl = ctypes.c_void_p()
-        _lib.check(L.fse_flags_alloc(ctypes.byref(fl)))
-        self.flags = fl
-        h_img = ctypes.create_string_buffer(_lib.FSE_IPC_HANDLE_BYTES)
-        h_flg = ctypes.create_string_buffer(_lib.FSE_IPC_HANDLE_BYTES)
-        _lib.check(L.fse_ipc_handle(ctypes.c_void_p(image_dev.data_ptr()), h_img))
-        _lib.check(L.fse_ipc_handle(fl, h_flg))
-        mine = (bytes(h_img.raw), bytes(h_flg.raw))
+        self.flags = None
+        mine = None
+        try:  # the handle exchange below is collective: always reach it
+            fl = ctypes.c_void_p()
+            _lib.check(L.fse_flags_alloc(ctypes.byref(fl)))
+            self.flags = fl
+            h_img = ctypes.create_string_buffer(_lib.FSE_IPC_HANDLE_BYTES)
+            h_flg = ctypes.create_string_buffer(_lib.FSE_IPC_HANDLE_BYTES)
+            _lib.check(L.fse_ipc_handle(ctypes.c_void_p(image_dev.data_ptr()), h_img))
+            _lib.check(L.fse_ipc_handle(fl, h_flg))
+            mine = (bytes(h_img.raw), bytes(h_flg.raw))
+        except Exception:
+            mine = None
         allh = [None] * world
         dist.all_gather_object(allh, mine, group=group)
+        if any(h is None for h in allh):
+            self._opened = []
+            self.close()
+            raise RuntimeError("peer mapping unavailable on some rank")
         self._opened = []
 
         def open_(h):
@@ -186,8 +195,12 @@ class PeerLink:
             self._opened.append(ptr)
             return ptr
 
-        self.up = (open_(allh[rank - 1][0]), open_(allh[rank - 1][1])) if rank > 0 else (None, None)
-        self.down = (open_(allh[rank + 1][0]), open_(allh[rank + 1][1])) if rank < world - 1 else (None, None)
+        try:
+            self.up = (open_(allh[rank - 1][0]), open_(allh[rank - 1][1])) if rank > 0 else (None, None)
+            self.down = (open_(allh[rank + 1][0]), open_(allh[rank + 1][1])) if rank < world - 1 else (None, None)
+        except Exception:
+            self.close()
+            raise
         self.epoch = 1  # flags start at 0, epochs at 1
 
     def attach(self, executor) -> None:
@@ -204,6 +217,25 @@ class PeerLink:
         if self.flags is not None:
             L.fse_flags_free(self.flags)
             self.flags = None
+
+
+def open_peer_link(image_dev, rank: int, world: int, dist, group=None):
+    """PeerLink on every rank, or None on every rank when any rank cannot map
+    its neighbours (no peer access between the devices, no IPC): the ranks
+    agree through one all_gather, and the caller falls back to the collective
+    exchange."""
+    link, ok = None, True
+    try:
+        link = PeerLink(image_dev, rank, world, dist, group)
+    except Exception:  # mapping failed on this rank
+        ok = False
+    flags = [None] * world
+    dist.all_gather_object(flags, ok, group=group)
+    if all(flags):
+        return link
+    if link is not None:
+        link.close()
+    return None
 
 
 def run_levels_p2p(executor, link: PeerLink) -> None:
@@ -238,8 +270,8 @@ def conceal_strips(image, mask, params: FseParams, precision: str = "fp32", orde
     msk_d = torch.from_numpy(mask).cuda()
     out_d = torch.empty_like(msk_d)
     ex = ShardExecutor(plan, bands[rank], img_d, msk_d, out_d, params, precision)
-    if world > 1 and transport == "p2p":
-        link = PeerLink(img_d, rank, world, dist, group)
+    link = open_peer_link(img_d, rank, world, dist, group) if world > 1 and transport == "p2p" else None
+    if link is not None:
         try:
             run_levels_p2p(ex, link)
             ex.close()
