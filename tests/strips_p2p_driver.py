@@ -21,15 +21,17 @@ def worker(rank, world, port, cfg, B, crop, q):
     F = {2: 32, 4: 64, 8: 128}[B]
     p = P.FseParams(d=14, iterations=40, block_size=B, fft_size=F)
     res = {}
-    for tr in ("p2p", "collective", "p2p"):
+    for tr, prec in (("p2p", "fp32"), ("collective", "fp32"), ("p2p", "fp32"), ("p2p", "fp64")):
         t = time.perf_counter()
-        out = strips.conceal_strips(img, mask, p, "fp32", transport=tr)
-        res.setdefault(tr, []).append((out, time.perf_counter() - t))
+        out = strips.conceal_strips(img, mask, p, prec, transport=tr)
+        res.setdefault((tr, prec), []).append((out, time.perf_counter() - t))
     if rank == 0:
-        whole, wm, _ = P.conceal(img, mask, p, precision="fp32")
         ok = {}
-        for tr, runs in res.items():
-            ok[tr] = all(np.array_equal(o[0], whole) and np.array_equal(o[1], wm) for o, _ in runs)
+        for prec in ("fp32", "fp64"):
+            whole, wm, _ = P.conceal(img, mask, p, precision=prec)
+            for (tr, pr), runs in res.items():
+                if pr == prec:
+                    ok[f"{tr}-{pr}"] = all(np.array_equal(o[0], whole) and np.array_equal(o[1], wm) for o, _ in runs)
         q.put(ok)
     dist.barrier()
     dist.destroy_process_group()
