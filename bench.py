@@ -2,15 +2,17 @@
 Mpixel/s, plus the fraction of the FP32 CUDA-core roofline).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--config 4] [--precision fp32] [--frames 64]
+                    [--config 4] [--precision fp64] [--frames 64] [--defaults]
 
 Workload (N=1 and every N): BASELINE config 4 — 64 independent 1920x1080
 synthetic luma frames (per-frame seeds), 20% mixed isolated+burst 16x16
 losses, FSE 4x4 / d=14 / FFT 64x64 / 100 iterations, rho=0.8, gamma=0.5,
-delta=0.2, optimized order, fp32.  Frame-parallel: rank r of N owns a
+delta=0.2, optimized order, fp64 (the parity path: identical picks to the
+reference, samples within 1e-6; --precision fp32 is the non-parity fast mode,
+also measured as a secondary record).  Frame-parallel: rank r of N owns a
 contiguous 64/N frame range (no data-path collective; scaling "strong": the
 64-frame job is fixed).  One step = the whole job once:
-    uint8->fp32 working copy -> host C++ plans of the rank's frames, the first
+    uint8->float working copy -> host C++ plans of the rank's frames, the first
     1/8 of them planned and launched before the rest is planned (overlapping the
     GPU) -> every dependency level of a chunk's frames as one sm_100a launch ->
     mask pass.
@@ -48,6 +50,14 @@ def counted_flops_per_block(iters: int, f1: int, f2: int) -> float:
     return 17.0 * iters * f1 * (f2 // 2 + 1)
 
 
+PARITY = {
+    "fp64": "parity path: every block's canonical pick sequence identical to the reference's and every "
+            "sample within 1e-6 (tests/test_gpu_conceal.py: 11 golden cases, full configs 1-4 and a 4K crop)",
+    "fp32": "NOT parity-green: fp32 fast mode; near-tie pick switches move some samples by more than 0.5 "
+            "(DESIGN.md §5) -- reported for reference only",
+}
+
+
 def args_():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -57,7 +67,12 @@ def args_():
     ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--block", type=int, default=4, choices=[2, 4, 8],
                     help="config 5 block size (FFT 32 / 64 / 128)")
-    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--precision", default="fp64", choices=["fp32", "fp64"],
+                    help="fp64 = the parity path (identical picks, 1e-6; the headline); fp32 = the "
+                         "non-parity fast mode (DESIGN.md §5)")
+    ap.add_argument("--defaults", action="store_true",
+                    help="the reference's default parameters (FseParams(): B=16, d=16, I=200, DFT = window "
+                         "size) -- the drop-in call conceal(image, mask) -- on the config's frames")
     ap.add_argument("--frames", type=int, default=64)
     ap.add_argument("--guard", default=None,
                     help="fp32 near-tie guard 'tau0,tau1' or 'off' (default: library default)")
@@ -91,7 +106,11 @@ def make_scenes(config, ids, threads=None):
         return list(ex.map(lambda f: synth.config_scene(config, f), ids))
 
 
-def workload_name(config, frames, precision):
+def workload_name(config, frames, precision, defaults=False):
+    if defaults:
+        return (f"config{config}: {frames if config == 4 else 1} x 1920x1080 synthetic luma, reference DEFAULT "
+                f"parameters FseParams() (B=16, d=16, I=200, rho=0.8, delta=0.2, gamma=0.5, DFT = window "
+                f"size 48x48 / clipped), optimized order, {precision}")
     if config == 4:
         return (f"config4: {frames} x 1920x1080 synthetic luma frames, 20% mixed 16x16 losses, "
                 f"FSE 4x4 / d=14 / FFT 64x64 / 100 it, optimized order, {precision}, frame-parallel")
@@ -157,14 +176,20 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ reference arm
 
+def oracle_params(O, iters, defaults):
+    """The oracle's Params for the bench workload (or the reference defaults)."""
+    if defaults:
+        return O.Params()  # fse.py:55-86 defaults, DFT = window size
+    return O.Params(d=D, rho=RHO, delta=DELTA, gamma=GAMMA, iterations=iters, block_size=B, fft_size=(F, F))
+
+
 def _ref_worker(job):
-    config, frame, iters, limit = job
+    config, frame, iters, limit, defaults = job
     from oracle import oracle as O
     from paper_2207_00233_b200 import synth
 
     img, mask = synth.config_scene(config, frame)
-    p = O.Params(d=D, rho=RHO, delta=DELTA, gamma=GAMMA, iterations=iters, block_size=B,
-                 fft_size=(F, F))
+    p = oracle_params(O, iters, defaults)
     kernel = "ref" if O.ref_kernel() is not None else "c"
     _, _, rep = O.conceal(img, mask, p, "optimized", kernel=kernel, block_limit=limit)
     return rep.blocks_processed, sample_seconds(rep), kernel
@@ -178,12 +203,12 @@ def sample_seconds(rep):
     return fit + rep.sched_time * rep.blocks_processed / max(1, rep.n_lossy)
 
 
-def cpu_reference(config, iters, cores, blocks_per_core, frames):
+def cpu_reference(config, iters, cores, blocks_per_core, frames, defaults=False):
     """Frame-parallel CPU run of the reference kernel: one process per core, each
     concealing the first `blocks_per_core` blocks of a different frame."""
     import multiprocessing as mp
 
-    jobs = [(config, f % (frames if config == 4 else 1), iters, blocks_per_core) for f in range(cores)]
+    jobs = [(config, f % (frames if config == 4 else 1), iters, blocks_per_core, defaults) for f in range(cores)]
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:
         res = pool.map(_ref_worker, jobs)
@@ -193,27 +218,37 @@ def cpu_reference(config, iters, cores, blocks_per_core, frames):
     return blocks, max(r[1] for r in res), res[0][2]
 
 
+def host_cores():
+    """(usable logical CPUs of this process, physical cores of the host)."""
+    cores = os.cpu_count() or 1
+    physical = None
+    try:
+        import psutil
+
+        cores = len(psutil.Process().cpu_affinity()) or cores
+        physical = psutil.cpu_count(logical=False)
+    except Exception:
+        pass
+    return cores, physical
+
+
 def run_reference(a, rank, world):
     if rank != 0:
         return
     from oracle import oracle as O
 
     iters = iterations_for(a.config)
-    cores = os.cpu_count() or 1
-    try:
-        import psutil
-
-        cores = len(psutil.Process().cpu_affinity()) or cores
-    except Exception:
-        pass
+    cores, physical = host_cores()
     per = max(20, 160 // max(1, iters // 100))  # ~0.75 s of CPU per core per step
+    if a.defaults:
+        per = 40  # 48x48 windows at 200 iterations: ~4 ms each
     kernel = "ref" if O.ref_kernel() is not None else "c"
     for _ in range(a.warmup):
-        cpu_reference(a.config, iters, cores, per // 4, a.frames)
+        cpu_reference(a.config, iters, cores, per // 4, a.frames, a.defaults)
     tot_b, tot_t = 0, 0.0
-    lost_px_per_block = B * B
+    lost_px_per_block = (16 if a.defaults else B) ** 2
     for _ in range(a.steps):
-        b, t, kernel = cpu_reference(a.config, iters, cores, per, a.frames)
+        b, t, kernel = cpu_reference(a.config, iters, cores, per, a.frames, a.defaults)
         tot_b += b
         tot_t += t
     value = tot_b / tot_t
@@ -225,9 +260,11 @@ def run_reference(a, rank, world):
         "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": 1000.0 * tot_t / a.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE generators)",
-        "config": {"workload": workload_name(a.config, a.frames, "fp64"), "sample": sample},
+        "config": {"workload": workload_name(a.config, a.frames, "fp64", a.defaults), "sample": sample},
         "lost_mpixel_per_s": value * lost_px_per_block / 1e6,
-        "cpu_baseline": {"value": value, "unit": "blocks/s", "cores": cores,
+        "cpu_baseline": {"value": value, "unit": "blocks/s", "cores": cores, "physical_cores": physical,
+                         "cores_note": "cores = processes run (one per usable logical CPU); physical_cores "
+                                       "= psutil.cpu_count(logical=False) on this host",
                          "kind": "reference" if kernel == "ref" else "port", "sample": sample},
         "e2e": {"value": value, "unit": "blocks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -284,6 +321,9 @@ def run_b200(a, rank, world, local_rank):
     iters = iterations_for(a.config)
     params = P.FseParams(d=D, rho=RHO, delta=DELTA, gamma=GAMMA, iterations=iters, block_size=B,
                          fft_size=F)
+    if a.defaults:
+        params = P.FseParams()  # reference defaults (fse.py:55-86), DFT = window size
+        iters = params.iterations
     ids = frame_ids(a.config, a.frames, rank, world)
     scenes = make_scenes(a.config, ids)
     imgs_h = torch.from_numpy(np.stack([s[0] for s in scenes])).pin_memory()
@@ -302,6 +342,19 @@ def run_b200(a, rank, world, local_rank):
     # work accounting from one plan set
     plans = P.build_plans(masks_np, params, "optimized", plan_threads)
     blocks_rank = sum(p.n_processed for p in plans)
+    # counted FLOPs of this rank's blocks: 17 I F1 (F2/2 + 1) each, F = the
+    # FFT size or (fft_size=None) the block's own window shape
+    if params.fft_size is None:
+        flop_rank = 0.0
+        for pl in plans:
+            blk = np.asarray([b for lv in pl.levels() for b in lv], dtype=np.int64)
+            r, c = blk // pl.cols, blk % pl.cols
+            Bq, dq = params.block_size, params.d
+            Mw = np.minimum(H, np.minimum(r * Bq + Bq, H) + dq) - np.maximum(0, r * Bq - dq)
+            Nw = np.minimum(W, np.minimum(c * Bq + Bq, W) + dq) - np.maximum(0, c * Bq - dq)
+            flop_rank += float(np.sum(17.0 * iters * Mw * (Nw // 2 + 1)))
+    else:
+        flop_rank = blocks_rank * counted_flops_per_block(iters, F, F)
     lost_px_rank = int((msks_h == 1).sum())
     levels = max(p.n_levels for p in plans)
     del plans
@@ -376,7 +429,6 @@ def run_b200(a, rank, world, local_rank):
 
     # roofline of the dominant kernel (the level launches): counted FLOPs per
     # block x blocks of this rank / summed CUDA-event time of the level launches
-    flop_blk = counted_flops_per_block(iters, F, F)
     peaks, sms = measure_peaks(torch, lib)
     fp32_peak = max(peaks["ffma"], peaks["ffma2"])
 
@@ -386,7 +438,7 @@ def run_b200(a, rank, world, local_rank):
         traffic = json.load(open(tpath))
 
     def roof(m, precision):
-        achieved = blocks_rank * flop_blk / (m["kernel_ms"] * 1e-3) / 1e12
+        achieved = flop_rank / (m["kernel_ms"] * 1e-3) / 1e12
         pk = fp32_peak if precision == "fp32" else peaks["dfma"]
         tr, detail = None, None
         blocks_per_launch = blocks_rank * a.steps / max(1, m["level_launches"])
@@ -406,7 +458,7 @@ def run_b200(a, rank, world, local_rank):
                 "bound_note": "FP32 (FP64) CUDA-core pipe roofline as BASELINE.json asks; the kernel "
                               "is compute/issue bound (>600 FLOP per HBM byte)",
                 "kernel": "fse_fast_kernel (one launch per dependency level)",
-                "flops_per_block": flop_blk,
+                "flops_per_block": flop_rank / max(1, blocks_rank),
                 "peak_source": (f"measured live on {sms} SMs by fse_fma_probe: FFMA {peaks['ffma']:.1f}, "
                                 f"FFMA2 {peaks['ffma2']:.1f}, DFMA {peaks['dfma']:.1f} TFLOP/s")}
 
@@ -436,12 +488,13 @@ def run_b200(a, rank, world, local_rank):
         from oracle import oracle as O
 
         img0, m0 = scenes[0]
-        p0 = O.Params(d=D, rho=RHO, delta=DELTA, gamma=GAMMA, iterations=iters, block_size=B,
-                      fft_size=(F, F))
+        p0 = oracle_params(O, iters, a.defaults)
         kern = "ref" if O.ref_kernel() is not None else "c"
-        _, _, rep = O.conceal(img0, m0, p0, "optimized", kernel=kern, block_limit=a.cpu_blocks)
+        _, _, rep = O.conceal(img0, m0, p0, "optimized", kernel=kern,
+                              block_limit=a.cpu_blocks // (8 if a.defaults else 1))
         secs = sample_seconds(rep)
         cpu = {"value": rep.blocks_processed / secs, "unit": "blocks/s", "cores": 1,
+               "host_physical_cores": host_cores()[1],
                "kind": "reference" if kern == "ref" else "port",
                "sample": f"first {rep.blocks_processed} of {rep.n_lossy} lossy blocks (optimized order) "
                          f"of frame 0: {rep.wall_time - rep.sched_time:.1f} s of fits + "
@@ -456,10 +509,11 @@ def run_b200(a, rank, world, local_rank):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32" if a.precision == "fp32" else "f64",
             "data": "synthetic (seeded BASELINE generators, paper_2207_00233_b200/synth.py)",
-            "config": {"workload": workload_name(a.config, a.frames, a.precision),
+            "config": {"workload": workload_name(a.config, a.frames, a.precision, a.defaults),
                        "frames": len(frame_ids(a.config, a.frames, 0, 1)), "H": H, "W": W,
-                       "block": B, "d": D, "fft": F, "iterations": iters, "rho": RHO,
-                       "delta": DELTA, "gamma": GAMMA, "order": "optimized",
+                       "block": params.block_size, "d": params.d, "fft": params.fft_size,
+                       "iterations": iters, "rho": params.rho, "delta": params.delta,
+                       "gamma": params.gamma, "order": "optimized",
                        "parallelism": f"frame-parallel x{world}",
                        "l2": "256 MiB buffer written every step (> 126 MB L2)"},
             "lost_mpixel_per_s": lost_px_all * a.steps / (head["ms"] * 1e-3) / 1e6,
@@ -468,6 +522,7 @@ def run_b200(a, rank, world, local_rank):
             "host_enqueue_ms_per_step": head["plan_ms"],
             "kernel_ms_per_step": head["kernel_ms"],
             "fp32_guard_fp64_redo_per_step": head["redo"],
+            "parity": PARITY[a.precision],
             "roofline": roof(head, a.precision),
             "gpu_launches": head["launches"],
             "e2e": e2e,
@@ -478,7 +533,8 @@ def run_b200(a, rank, world, local_rank):
             line[other_prec] = {
                 "value": blocks_all * a.steps / (other["ms"] * 1e-3), "unit": "blocks/s",
                 "ms_per_step": other["ms"] / a.steps, "kernel_ms_per_step": other["kernel_ms"],
-                "roofline": roof(other, other_prec), "gpu_launches": other["launches"]}
+                "roofline": roof(other, other_prec), "gpu_launches": other["launches"],
+                "parity": PARITY[other_prec]}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -596,20 +652,13 @@ def run_strips_bench(a, rank, world, local_rank):
         bands = strips.band_partition(processed.sum(axis=1), world, R)
         stats["plan_ms"] = 1e3 * (time.perf_counter() - t0)
         stats["blocks"] = plan.n_processed
-        ex = strips.ShardExecutor(plan, bands[rank], work, msk, out, params, "fp32")
-        if link is not None:
-            strips.run_levels_p2p(ex, link)
+        ex = strips.ShardExecutor(plan, bands[rank], work, msk, out, params, a.precision)
+        if link is not None and strips.run_levels_p2p(ex, link, dist, grp):
             stats["halo_msgs"] = 0
+            stats["fused"] = True
         else:
-            flags_all = [ex.flags]
-            if world > 1:
-                dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
-                t = torch.as_tensor(ex.flags, dtype=torch.int32, device=dev)
-                g = [torch.empty_like(t) for _ in range(world)]
-                dist.all_gather(g, t)
-                flags_all = [x.cpu().numpy() for x in g]
-            stats["halo_msgs"] = strips.run_levels(ex, work, rank, world, bands, flags_all, ex.n_levels, R,
-                                                   Bk, H, dist, grp)
+            stats["fused"] = False
+            stats["halo_msgs"] = strips.run_levels_collective(ex, work, rank, world, bands, R, Bk, H, dist, grp)
         stats["levels"] = ex.n_levels
         ex.close()
         if world > 1:  # gather the bands to rank 0 (gloo: through host buffers)

@@ -214,13 +214,19 @@ int fse_ipc_close(void *dev_ptr);
 int fse_flags_alloc(uint32_t **flags);
 int fse_flags_free(uint32_t *flags);
 /* neighbours' frames and flags (NULL = no neighbour on that side), this
- * rank's own flags, and the run's epoch (1, 2, 3, ... identical on every
- * rank; flag values of one epoch never satisfy another's waits).  A run
- * starting at level 0 first signals "frame initialised" and waits for the
- * neighbours' signal, so work queued before it on the stream (a frame reset)
- * precedes every peer store into this frame. */
+ * rank's own flags, and the run's flag base (identical on every rank).  The
+ * run's flag values lie in [base, base + n_levels]; a caller reusing the
+ * flags passes, for each run, a base above the previous run's last value
+ * (base_next = base + n_levels + 1; flags start at 0, so the first base is
+ * >= 1), so values of one run never satisfy another's waits whatever the
+ * runs' level counts.  A run starting at level 0 first signals "frame
+ * initialised" and waits for the neighbours' signal, so work queued before it
+ * on the stream (a frame reset) precedes every peer store into this frame.
+ * All-NULL peers detach the shard (always allowed).  FSE_ENOTSUP when the
+ * shard cannot fuse the exchange (not the fast kernel, or several frames):
+ * callers then agree on the collective exchange (strips.conceal_strips). */
 int fse_shard_set_peers(FseShard *shard, void *up_image, uint32_t *up_flags, void *down_image,
-                        uint32_t *down_flags, uint32_t *own_flags, uint32_t epoch);
+                        uint32_t *down_flags, uint32_t *own_flags, uint32_t base);
 
 /* Output epilogue over n frames of npix samples each (device pointers, frames
  * contiguous): out_u8 (or NULL) = floor(clip(x, 0, 255) + 0.5), the rounding

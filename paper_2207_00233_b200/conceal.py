@@ -145,7 +145,9 @@ class DeviceContext:
     def decay(cls, params: FseParams, dim: int):
         import torch
 
-        key = (params.rho, dim)
+        # one table per device: a pointer from another device's memory would
+        # reach the kernel of a call on this one
+        key = (torch.cuda.current_device(), params.rho, dim)
         t = cls._cache.get(key)
         if t is None:
             t = torch.from_numpy(decay_table(params.rho, dim)).cuda()
@@ -301,7 +303,7 @@ def _batch_buffers(n, H, W, in_dtype, tdt):
 
 
 def conceal_batch(images, masks, params: FseParams | None = None, order: str = OPTIMIZED,
-                  precision: str = "fp32", plan_threads: int = 0, reports: bool = True,
+                  precision: str = "fp64", plan_threads: int = 0, reports: bool = True,
                   out_images=None, out_masks=None):
     """Frame-parallel concealment of equally sized frames: one plan per frame
     (C++ threads, overlapped with the upload), every dependency level of every

@@ -31,27 +31,27 @@ static thread_local TimingState g_timing;
 
 // fp32 near-tie guard thresholds (fse_fast.cuh): redo in fp64 when
 // e1 - e2 <= (tau0 + tau1 * it) * e1.  Negative tau0 disables the guard.
-static double g_tau0 = -1.0, g_tau1 = 0.0;
+static std::atomic<double> g_tau0{-1.0}, g_tau1{0.0};
 
 // Persistent dataflow launch instead of one launch per level.  Off by default:
 // measured on config 4 it ties the level launches (fp32) or loses 5% (fp64) —
 // the critical path is the DAG depth either way and the level launches already
 // keep ~97% wave efficiency.  FSE_DATAFLOW=1 or fse_set_dataflow(1) selects it.
-static bool g_dataflow = [] {
+static std::atomic<bool> g_dataflow{[] {
     const char *e = getenv("FSE_DATAFLOW");
     return e && e[0] == '1';
-}();
-bool dataflow_enabled() { return g_dataflow; }
+}()};
+bool dataflow_enabled() { return g_dataflow.load(std::memory_order_relaxed); }
 
 // Frame groups of one fse_conceal_frames call run their level sequences on
 // separate forked streams, so the partial last wave of one group's level
 // overlaps the next level of another (the levels of different frames are
 // independent).  FSE_GROUPS=1 restores one launch sequence.
-static int g_groups = [] {
+static std::atomic<int> g_groups{[] {
     const char *e = getenv("FSE_GROUPS");
     const int v = e ? atoi(e) : 2;
     return std::max(1, std::min(v, 8));
-}();
+}()};
 
 // Pinned host staging buffers for the session uploads (frame table, ranks,
 // level entry lists; tens of MB for a 64-frame batch).  A pageable source
@@ -158,7 +158,7 @@ static cudaStream_t group_stream(int g) {
     if (!pool[dev][g]) cudaStreamCreateWithFlags(&pool[dev][g], cudaStreamNonBlocking);
     return pool[dev][g];
 }
-static long long g_redo_total = 0;
+static std::atomic<long long> g_redo_total{0};
 
 // FP32 FMA throughput probe: 8 independent FFMA chains per thread.
 __global__ void fma_probe_kernel(float *out, int iters, float a, float b) {
@@ -393,9 +393,7 @@ int fse_set_groups(int32_t n) {
 }
 
 int64_t fse_guard_redo_count(int32_t reset) {
-    const long long v = fse::g_redo_total;
-    if (reset) fse::g_redo_total = 0;
-    return v;
+    return reset ? fse::g_redo_total.exchange(0) : fse::g_redo_total.load();
 }
 
 int64_t fse_launch_count(int32_t reset) {
@@ -651,8 +649,8 @@ static int session_open(int32_t n, FsePlan *const *plans, void *const *images, c
         f.iterations = a.iterations;
         f.gamma = a.gamma;
         f.picks = a.picks;
-        f.tau0 = (float)g_tau0;
-        f.tau1 = (float)g_tau1;
+        f.tau0 = (float)g_tau0.load();
+        f.tau1 = (float)g_tau1.load();
         f.R = S->R;
     }
     *out = S;
@@ -889,7 +887,7 @@ int fse_conceal_frames(int32_t n, FsePlan *const *plans, void *const *images,
     cudaStream_t s = (cudaStream_t)stream;
     FseShard *S = nullptr;
     // the dataflow executor walks one level-ordered list: one group
-    const int groups = fse::dataflow_enabled() ? 1 : fse::g_groups;
+    const int groups = fse::dataflow_enabled() ? 1 : fse::g_groups.load();
     int rc = fse::session_open(n, plans, images, masks, masks_out, p, dtype, decay, decay_dim, picks, 0,
                                plans[0]->p.rows, groups, s, &S);
     if (rc) return rc;
@@ -998,10 +996,16 @@ int fse_flags_free(uint32_t *flags) {
 }
 
 int fse_shard_set_peers(FseShard *sh, void *up_image, uint32_t *up_flags, void *down_image,
-                        uint32_t *down_flags, uint32_t *own_flags, uint32_t epoch) {
+                        uint32_t *down_flags, uint32_t *own_flags, uint32_t base) {
     if (!sh) return fail(FSE_EINVAL, "NULL shard");
     if ((up_image == nullptr) != (up_flags == nullptr) || (down_image == nullptr) != (down_flags == nullptr))
         return fail(FSE_EINVAL, "a neighbour needs both its frame and its flags");
+    if (!up_image && !down_image) {  // detach: plain level launches again
+        sh->f.peer_up = sh->f.peer_down = nullptr;
+        sh->sig_up = sh->sig_down = sh->own_flags = nullptr;
+        sh->peers = false;
+        return FSE_OK;
+    }
     if ((up_image || down_image) && !own_flags) return fail(FSE_EINVAL, "NULL own flags");
     if (!sh->fast || sh->guard || sh->n != 1)
         return fail(FSE_ENOTSUP, "fused halo exchange needs the fast kernel (F = 32/64/128), no guard, one frame");
@@ -1014,8 +1018,9 @@ int fse_shard_set_peers(FseShard *sh, void *up_image, uint32_t *up_flags, void *
     sh->sig_up = up_flags ? up_flags + 1 : nullptr;        // the upper neighbour's "from below"
     sh->sig_down = down_flags ? down_flags + 0 : nullptr;  // the lower neighbour's "from above"
     sh->own_flags = own_flags;
-    if (epoch == 0) return fail(FSE_EINVAL, "epochs start at 1 (flags start at 0)");
-    sh->base = epoch * (uint32_t)(sh->n_levels + 1);
+    if (base == 0) return fail(FSE_EINVAL, "the flag base starts at 1 (flags start at 0)");
+    if (base > 0x7FFFFFFFu - (uint32_t)sh->n_levels) return fail(FSE_EINVAL, "flag base overflows");
+    sh->base = base;
     sh->peers = up_image || down_image;
     return FSE_OK;
 }

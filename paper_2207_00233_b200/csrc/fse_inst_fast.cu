@@ -3,10 +3,57 @@
 #include <cstdlib>
 #include <algorithm>
 #include <string>
+#include <type_traits>
 
 #include "fse_fast.cuh"
 
 namespace fse {
+
+// Per-device launch state.  cudaFuncSetAttribute applies to the current
+// device only, so the "largest dynamic shared memory configured" record of
+// each kernel is kept per device (a process may drive several GPUs), and so
+// is the SM count.
+constexpr int kMaxDev = 64;
+static int current_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return dev;
+}
+static int device_sms(int dev) {
+    static std::atomic<int> cache[kMaxDev] = {};
+    if (dev < 0 || dev >= kMaxDev) dev = 0;
+    int v = cache[dev].load(std::memory_order_relaxed);
+    if (v <= 0) {
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) {
+            cudaGetLastError();
+            v = 148;
+        }
+        cache[dev].store(v, std::memory_order_relaxed);
+    }
+    return v;
+}
+// Raise kern's dynamic shared-memory limit on the current device to `bytes`
+// (once per kernel, device and size).  Tag: one static per kernel instance.
+template <class... K> struct KTag {};  // one type per kernel instance
+template <class Tag>
+static int ensure_smem(const void *kern, size_t bytes) {
+    static std::atomic<size_t> configured[kMaxDev] = {};
+    const int dev = current_device();
+    std::atomic<size_t> &c = configured[dev < kMaxDev ? dev : 0];
+    if (bytes <= c.load(std::memory_order_acquire)) return FSE_OK;
+    int optin = 0;
+    FSE_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    if (bytes > (size_t)optin)
+        return fail(FSE_ENOTSUP, "fast kernel needs " + std::to_string(bytes) + " B of shared memory");
+    FSE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    size_t cur = c.load(std::memory_order_relaxed);
+    while (bytes > cur && !c.compare_exchange_weak(cur, bytes)) {
+    }
+    return FSE_OK;
+}
 
 // F = 64: 66 row segments of the half plane over 6 warps -> 11 bins per thread
 // (4 warps / 17 bins measured 5% slower: fewer warps to hide latency).
@@ -61,6 +108,7 @@ template <typename T> using Fast128 = FastCfg<T, 128, FSE_F128_NW>;
 #define FSE_F128T_NW FSE_F128_NW
 #endif
 using Fast128T = FastCfg<float, 128, FSE_F128T_NW, true, 0, 1, true>;
+#ifdef FSE_WITH_CLUSTER  // experiment, measured slower everywhere: not in the default build
 // Cluster variants for levels narrower than the GPU: one window over CL SMs.
 template <typename T, int CL> using Fast64C = FastCfg<T, 64, 6, sizeof(T) == 4, 0, CL>;
 template <typename T, int CL> using Fast32C = FastCfg<T, 32, 6, true, 0, CL>;
@@ -82,11 +130,7 @@ template <class C>
 static int launch_cluster(const FastArgs &a, int windows, int Mmax, int Nmax, int model_n, cudaStream_t s) {
     const FastLayout L = fast_layout<typename C::T>(C::F, C::NWT, Mmax, Nmax, model_n, a.iterations, C::EXT);
     auto kern = fse_fast_cluster_kernel<C>;
-    static thread_local size_t configured = 0;
-    if (L.total > configured) {
-        FSE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-        configured = L.total;
-    }
+    if (int rc = ensure_smem<KTag<C, std::integral_constant<int, 100>>>((const void *)kern, L.total)) return rc;
     if (windows > 0) {
         kern<<<windows * C::CL, C::NT, L.total, s>>>(a, L);
         FSE_CUDA_TRY(cudaGetLastError());
@@ -94,6 +138,9 @@ static int launch_cluster(const FastArgs &a, int windows, int Mmax, int Nmax, in
     }
     return FSE_OK;
 }
+#else
+bool cluster_levels() { return false; }
+#endif
 // (A 22-warp / 3-bin "latency" variant for levels narrower than the GPU was
 // measured 20% slower on configs 1-2: per-iteration overhead grows with warps.)
 
@@ -110,16 +157,7 @@ static int launch(const FastArgs &a, int grid, int Mmax, int Nmax, int model_n, 
     L.total += FSE_SMEM_PAD;  // dev: occupancy sensitivity experiments
 #endif
     auto kern = fse_fast_kernel<C, MODE, GUARD>;
-    static thread_local size_t configured = 0;  // largest dynamic smem size set so far
-    if (L.total > configured) {
-        int dev = 0, optin = 0;
-        FSE_CUDA_TRY(cudaGetDevice(&dev));
-        FSE_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-        if (L.total > (size_t)optin)
-            return fail(FSE_ENOTSUP, "fast kernel needs " + std::to_string(L.total) + " B of shared memory");
-        FSE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-        configured = L.total;
-    }
+    if (int rc = ensure_smem<KTag<C, std::integral_constant<int, MODE>, std::integral_constant<bool, GUARD>>>((const void *)kern, L.total)) return rc;
     if (grid > 0) {
         kern<<<grid, C::NT, L.total, s>>>(a, L);
         FSE_CUDA_TRY(cudaGetLastError());
@@ -132,16 +170,10 @@ template <class C>
 static int launch_redo(const FastArgs &a, int max_entries, int Mmax, int Nmax, int model_n, cudaStream_t s) {
     const FastLayout L = fast_layout<typename C::T>(C::F, C::NWT, Mmax, Nmax, model_n, a.iterations, C::EXT);
     auto kern = fse_fast_redo_kernel<C, float>;
-    static thread_local size_t configured = 0;
-    static thread_local int per_sm = 0, sms = 0;
-    if (L.total > configured) {
-        int dev = 0;
-        FSE_CUDA_TRY(cudaGetDevice(&dev));
-        FSE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-        FSE_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::NT, L.total));
-        FSE_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        configured = L.total;
-    }
+    if (int rc = ensure_smem<KTag<C, std::integral_constant<int, 101>>>((const void *)kern, L.total)) return rc;
+    int per_sm = 0;
+    const int sms = device_sms(current_device());
+    FSE_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::NT, L.total));
     int grid = std::min(max_entries, std::max(1, per_sm) * std::max(1, sms));
     if (grid > 0) {
         kern<<<grid, C::NT, L.total, s>>>(a, L);
@@ -155,16 +187,10 @@ template <class C, typename IT>
 static int launch_dataflow(const FastArgs &a, int Mmax, int Nmax, int model_n, cudaStream_t s) {
     const FastLayout L = fast_layout<typename C::T>(C::F, C::NWT, Mmax, Nmax, model_n, a.iterations, C::EXT);
     auto kern = fse_fast_dataflow_kernel<C, IT>;
-    static thread_local size_t configured = 0;
-    static thread_local int per_sm = 0, sms = 0;
-    if (L.total > configured) {
-        int dev = 0;
-        FSE_CUDA_TRY(cudaGetDevice(&dev));
-        FSE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-        FSE_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::NT, L.total));
-        FSE_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        configured = L.total;
-    }
+    if (int rc = ensure_smem<KTag<C, IT, std::integral_constant<int, 102>>>((const void *)kern, L.total)) return rc;
+    int per_sm = 0;
+    const int sms = device_sms(current_device());
+    FSE_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::NT, L.total));
     if (per_sm < 1) return fail(FSE_ENOTSUP, "dataflow kernel does not fit on an SM");
     const int grid = std::max(1, std::min(a.total, per_sm * sms));
     {
@@ -195,15 +221,8 @@ int fast_dataflow(int dtype, int F, const FastArgs &a, int Mmax, int Nmax, int m
 
 int fast_level(int dtype, int F, bool guard, const FastArgs &a, int grid, int Mmax, int Nmax,
                int model_n, cudaStream_t s) {
-    static const int sms = [] {
-        int dev = 0, v = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess ||
-            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
-            cudaGetLastError();
-            return 148;
-        }
-        return v;
-    }();
+    const int sms = device_sms(current_device());
+#ifdef FSE_WITH_CLUSTER
     // narrow level: give each window 4 (or 2) SMs as a cluster
     if (!guard && cluster_levels() && (F == 64 || F == 32) && grid * 2 <= sms) {
         const bool four = cluster_mode() == 4 || (cluster_mode() != 2 && grid * 4 <= sms);
@@ -220,6 +239,7 @@ int fast_level(int dtype, int F, bool guard, const FastArgs &a, int grid, int Mm
         return four ? launch_cluster<Fast32C<double, 4>>(a, grid, Mmax, Nmax, model_n, s)
                     : launch_cluster<Fast32C<double, 2>>(a, grid, Mmax, Nmax, model_n, s);
     }
+#endif
     if (dtype == FSE_F32) {
         const bool narrow = grid < track_below(sms);
         if (F == 128)

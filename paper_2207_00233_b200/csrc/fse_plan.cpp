@@ -84,24 +84,33 @@ void init_counts_impl(const uint8_t *lossy, int rows, int cols, int32_t *counts)
     }
 }
 
+// Largest pending count schedule_impl accepts (one bucket per value); the
+// reference's init_counts produces at most 8 + 5.
+constexpr int kMaxCount = 1 << 14;
+
 // schedule.py:60-105 with a bucket queue: one bitset of pending blocks per
 // count value, scanned in row-major order for the current minimum.  Selection
 // of a whole batch happens before any commit, as in select_batch/commit_batch.
-void schedule_impl(const int32_t *counts_in, int rows, int cols,
-                   std::vector<int32_t> &ptr, std::vector<int32_t> &blocks) {
+
+int schedule_impl(const int32_t *counts_in, int rows, int cols,
+                  std::vector<int32_t> &ptr, std::vector<int32_t> &blocks) {
     const int nb = rows * cols;
     const int words = (nb + 63) / 64;
-    // counts fit in int8: at most 8 + 5 at the start, done blocks drift down
-    // to -1 - 8 (schedule.py:85-94); one byte per block keeps them in cache
-    std::vector<int8_t> cnt(nb);
-    for (int b = 0; b < nb; ++b) cnt[b] = (int8_t)std::max(-128, std::min(127, (int)counts_in[b]));
+    // Pending counts (>= 0) fit in int16; everything below 0 is done and its
+    // exact value never matters again (select_batch only looks at counts >= 0,
+    // schedule.py:69-70), so done blocks are kept at -1 instead of drifting.
     int maxc = 0;
     long pending = 0;
     for (int b = 0; b < nb; ++b)
-        if (cnt[b] >= 0) {
-            maxc = std::max(maxc, (int)cnt[b]);
+        if (counts_in[b] >= 0) {
+            if (counts_in[b] > kMaxCount)
+                return fail(FSE_EINVAL, "count " + std::to_string(counts_in[b]) + " above the supported " +
+                                            std::to_string(kMaxCount));
+            maxc = std::max(maxc, (int)counts_in[b]);
             ++pending;
         }
+    std::vector<int16_t> cnt(nb);
+    for (int b = 0; b < nb; ++b) cnt[b] = (int16_t)(counts_in[b] >= 0 ? counts_in[b] : -1);
     // bucket c: bitset of pending blocks with count c; summary: bitset of its
     // non-zero words, so a row-major scan skips empty stretches 64 words at a
     // time.  The count is the fast index of both arrays: a neighbour's move
@@ -170,13 +179,17 @@ void schedule_impl(const int32_t *counts_in, int rows, int cols,
             taken[b] = 0;
             --pending;
         }
+        // commit_batch (schedule.py:85-94): every neighbour's count drops by
+        // one.  A pending block whose count falls below 0 is done from then on
+        // (never selected: select_batch's pending set is counts >= 0); with
+        // init_counts' counts that cannot happen (a pending count is at least
+        // its number of pending lossy neighbours), with caller-supplied ones it
+        // can, as in the reference.
         auto release = [&](int o) {
             if (cnt[o] >= 0) {
                 del(cnt[o], o);
-                --cnt[o];
-                add(cnt[o], o);
-            } else {
-                --cnt[o];  // done blocks drift below -1 (schedule.py:85-94)
+                if (--cnt[o] >= 0) add(cnt[o], o);
+                else --pending;
             }
         };
         for (int b : batch) {
@@ -200,6 +213,7 @@ void schedule_impl(const int32_t *counts_in, int rows, int cols,
         if (prof) t_com += ms(q1, now());
     }
     if (prof) fprintf(stderr, "plan   schedule loop: select %.1f ms, commit %.1f ms\n", t_sel, t_com);
+    return FSE_OK;
 }
 
 struct Geometry {
@@ -322,7 +336,8 @@ int build_one(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p, in
         std::vector<int32_t> counts(nb);
         init_counts_impl(lossy.data(), rows, cols, counts.data());
         lap("init_counts");
-        schedule_impl(counts.data(), rows, cols, ph_ptr, ph_blocks);
+        rc = schedule_impl(counts.data(), rows, cols, ph_ptr, ph_blocks);
+        if (rc) return rc;
     } else {
         ph_ptr.assign(1, 0);
         for (int b = 0; b < nb; ++b)
@@ -495,7 +510,7 @@ int fse_schedule_all(const int32_t *counts, int32_t rows, int32_t cols, int32_t 
         return fail(FSE_EINVAL, "bad arguments");
     std::vector<int32_t> vp, vb;
     try {
-        fse::schedule_impl(counts, rows, cols, vp, vb);
+        if (int rc = fse::schedule_impl(counts, rows, cols, vp, vb)) return rc;
     } catch (const std::exception &e) {
         return fail(FSE_ENOMEM, e.what());
     }

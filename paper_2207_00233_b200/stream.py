@@ -7,8 +7,13 @@ batches, and each batch runs through a pipeline whose stages overlap with the
 neighbouring batches' --
 
     host:   copy into a pinned slot -> plan (C++ threads)
-    copy:   upload batch k+1          | download batch k-1
-    main:               levels of batch k (every frame's level l in one launch)
+    up:     upload batch k+1
+    down:   download batch k-1 (waits only for batch k-1's levels)
+    main:   levels of batch k (every frame's level l in one launch)
+
+Uploads and downloads use separate streams: on one in-order copy stream the
+next batch's upload would queue behind the previous batch's download, which
+waits for that batch's levels, and the GPU would idle between batches.
 
 A background thread plans and enqueues batches in order, so ``push`` returns
 at once; concealed frames come back in push order, from ``push`` (whatever has
@@ -35,7 +40,7 @@ class ConcealStream:
     flight (pinned host slots and device buffers are allocated once).
     """
 
-    def __init__(self, params: FseParams | None, shape, batch: int = 16, precision: str = "fp32",
+    def __init__(self, params: FseParams | None, shape, batch: int = 16, precision: str = "fp64",
                  order: str = OPTIMIZED, depth: int = 3, plan_threads: int = 0, in_dtype=np.uint8):
         import torch
 
@@ -60,7 +65,8 @@ class ConcealStream:
         itd = torch.from_numpy(np.zeros(1, dtype=self._in_np)).dtype
         self.device = torch.cuda.current_device()
         self._main = torch.cuda.Stream(device=self.device)
-        self._copy = torch.cuda.Stream(device=self.device)
+        self._up = torch.cuda.Stream(device=self.device)
+        self._down = torch.cuda.Stream(device=self.device)
         # slot = pinned inputs + outputs on the host, frames + masks on the device
         self._slots = []
         for _ in range(depth):
@@ -95,14 +101,14 @@ class ConcealStream:
             s = self._slots[i]
             n = s["n"]
             try:
-                with torch.cuda.stream(self._copy):  # upload (pinned -> device), widen
+                with torch.cuda.stream(self._up):  # upload (pinned -> device), widen
                     if s["in_d"] is None:
                         s["img_d"][:n].copy_(s["img_h"][:n], non_blocking=True)
                     else:
                         s["in_d"][:n].copy_(s["img_h"][:n], non_blocking=True)
                         s["img_d"][:n].copy_(s["in_d"][:n])
                     s["msk_d"][:n].copy_(s["msk_h"][:n], non_blocking=True)
-                    up = self._copy.record_event()
+                    up = self._up.record_event()
                 plans = build_plans(list(s["msk_h"][:n].numpy()), self.params, self.order, self.plan_threads)
                 self._main.wait_event(up)
                 with torch.cuda.stream(self._main):
@@ -115,12 +121,12 @@ class ConcealStream:
                 # allocator recycles them once the caller drops the frames)
                 s["out_h"] = torch.empty((n,) + self.shape, dtype=self._tdt, pin_memory=True)
                 s["omsk_h"] = torch.empty((n,) + self.shape, dtype=torch.uint8, pin_memory=True)
-                with torch.cuda.stream(self._copy):  # download (device -> pinned)
-                    self._copy.wait_event(ran)
+                with torch.cuda.stream(self._down):  # download (device -> pinned)
+                    self._down.wait_event(ran)
                     s["out_h"][:n].copy_(s["img_d"][:n], non_blocking=True)
                     s["omsk_h"][:n].copy_(s["omsk_d"][:n], non_blocking=True)
                     ev = torch.cuda.Event()
-                    ev.record(self._copy)
+                    ev.record(self._down)
                 s["plans"] = plans  # keep the plans alive until the batch is done
                 s["done"] = ev
             except Exception as e:  # surfaced to the caller on the next push/flush

@@ -201,13 +201,24 @@ class PeerLink:
         except Exception:
             self.close()
             raise
-        self.epoch = 1  # flags start at 0, epochs at 1
+        # flag values of successive runs: [base, base + n_levels], each run's
+        # base above the previous run's last value (flags start at 0), so a
+        # run with fewer levels than the last one never sees stale values
+        self.next_base = 1
 
-    def attach(self, executor) -> None:
-        """Route this shard's halos through peer memory for its next run."""
-        _lib.check(_lib.lib().fse_shard_set_peers(executor.handle, self.up[0], self.up[1], self.down[0],
-                                                  self.down[1], self.flags, self.epoch))
-        self.epoch += 1
+    def attach(self, executor) -> int:
+        """Route this shard's halos through peer memory for its next run.
+        Returns the C status (FSE_ENOTSUP when the shard cannot fuse the
+        exchange) instead of raising, so the ranks can agree on a fallback."""
+        rc = _lib.lib().fse_shard_set_peers(executor.handle, self.up[0], self.up[1], self.down[0],
+                                            self.down[1], self.flags, self.next_base)
+        if rc == 0:
+            self.next_base += executor.n_levels + 1
+        return rc
+
+    @staticmethod
+    def detach(executor) -> None:
+        _lib.check(_lib.lib().fse_shard_set_peers(executor.handle, None, None, None, None, None, 0))
 
     def close(self) -> None:
         L = _lib.lib()
@@ -238,13 +249,54 @@ def open_peer_link(image_dev, rank: int, world: int, dist, group=None):
     return None
 
 
-def run_levels_p2p(executor, link: PeerLink) -> None:
-    """The whole level sequence of one shard with the fused exchange."""
-    link.attach(executor)
+def attach_all(executor, link: PeerLink, dist, group=None) -> bool:
+    """Attach every rank's shard to its peers, or none: the fused exchange
+    needs the fast kernel on every rank (fse_shard_set_peers answers
+    FSE_ENOTSUP otherwise, e.g. fp64 at F = 128 or fft_size=None), so the
+    ranks agree through one all_gather and fall back to the collective
+    exchange together."""
+    rc = link.attach(executor)
+    if rc not in (0, _lib.FSE_ENOTSUP):
+        _lib.check(rc)
+    oks = [None] * link.world
+    dist.all_gather_object(oks, rc == 0, group=group)
+    if all(oks):
+        return True
+    if rc == 0:
+        PeerLink.detach(executor)
+    return False
+
+
+def run_levels_p2p(executor, link: PeerLink, dist=None, group=None) -> bool:
+    """The whole level sequence of one shard with the fused exchange.  With
+    `dist`, the ranks first agree (attach_all); returns False, having run
+    nothing, when some rank's shard cannot fuse the exchange."""
+    if dist is not None:
+        if not attach_all(executor, link, dist, group):
+            return False
+    else:
+        _lib.check(link.attach(executor))
     _lib.check(_lib.lib().fse_shard_run(executor.handle, 0, executor.n_levels, executor.stream))
+    return True
 
 
-def conceal_strips(image, mask, params: FseParams, precision: str = "fp32", order: str = "optimized",
+def run_levels_collective(executor, image_dev, rank, world, bands, R, B, H, dist, group=None) -> int:
+    """The per-level send/recv protocol (run_levels) with the edge flags of
+    every rank gathered first."""
+    import torch
+
+    flags_all = [executor.flags]
+    if world > 1:
+        dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+        t = torch.as_tensor(executor.flags, dtype=torch.int32, device=dev)
+        gathered = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(gathered, t, group=group)
+        flags_all = [g.cpu().numpy() for g in gathered]
+    return run_levels(executor, image_dev, rank, world, bands, flags_all, executor.n_levels, R, B, H, dist,
+                      group)
+
+
+def conceal_strips(image, mask, params: FseParams, precision: str = "fp64", order: str = "optimized",
                    group=None, gather: bool = True, transport: str = "p2p"):
     """Conceal one frame on all ranks of the default process group (one GPU per
     rank).  Returns (image, mask) numpy arrays on rank 0 when gather=True (other
@@ -271,23 +323,18 @@ def conceal_strips(image, mask, params: FseParams, precision: str = "fp32", orde
     out_d = torch.empty_like(msk_d)
     ex = ShardExecutor(plan, bands[rank], img_d, msk_d, out_d, params, precision)
     link = open_peer_link(img_d, rank, world, dist, group) if world > 1 and transport == "p2p" else None
+    fused = False
     if link is not None:
         try:
-            run_levels_p2p(ex, link)
-            ex.close()
-            torch.cuda.synchronize()
-            dist.barrier(group=group)  # every rank's peer stores have landed
+            fused = run_levels_p2p(ex, link, dist, group)
+            if fused:
+                ex.close()
+                torch.cuda.synchronize()
+                dist.barrier(group=group)  # every rank's peer stores have landed
         finally:
             link.close()
-    else:
-        flags_all = [ex.flags]
-        if world > 1:
-            dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
-            t = torch.as_tensor(ex.flags, dtype=torch.int32, device=dev)
-            gathered = [torch.empty_like(t) for _ in range(world)]
-            dist.all_gather(gathered, t, group=group)
-            flags_all = [g.cpu().numpy() for g in gathered]
-        run_levels(ex, img_d, rank, world, bands, flags_all, ex.n_levels, R, B, H, dist, group)
+    if not fused:
+        run_levels_collective(ex, img_d, rank, world, bands, R, B, H, dist, group)
         ex.close()
     lo, hi = bands[rank]
     y0, y1 = lo * B, min(H, hi * B)

@@ -88,3 +88,55 @@ def emulate_levels(image, mask, B, d, rho, delta, gamma, iterations, fft, ranks,
     done = ranks[owner] != np.iinfo(np.int32).max
     out_mask[(mask == O.LOST) & done] = O.RECONSTRUCTED
     return img, out_mask
+
+
+# ---- large golden fixtures (tests/golden/make_golden_large.py)
+
+def large_case(g):
+    """Inputs of a large golden case, regenerated from the seeded generator,
+    plus its parameters (FseParams keyword arguments) and fft size."""
+    from paper_2207_00233_b200 import synth
+
+    img, mask = synth.config_scene(int(g["config"]), int(g["frame"]))
+    r0, r1, c0, c1 = (int(x) for x in g["crop"])
+    if r1 > r0:
+        img, mask = img[r0:r1, c0:c1].copy(), mask[r0:r1, c0:c1].copy()
+    assert [int(img.astype(np.int64).sum()), int(mask.astype(np.int64).sum())] == g["input_sums"].tolist()
+    d, rho, delta, gamma, iters, B = g["params"].tolist()
+    fft = tuple(int(x) for x in g["fft"])
+    kw = dict(d=int(d), rho=rho, delta=delta, gamma=gamma, iterations=int(iters), block_size=int(B))
+    return img, mask, kw, (None if fft == (0, 0) else fft)
+
+
+def window_shapes(H, W, B, d, blocks):
+    """(M, N) of each block's window (grid.py:108-135: block +- d, clipped)."""
+    cols = -(-W // B)
+    r, c = np.asarray(blocks) // cols, np.asarray(blocks) % cols
+    r0, c0 = r * B, c * B
+    M = np.minimum(H, np.minimum(r0 + B, H) + d) - np.maximum(0, r0 - d)
+    N = np.minimum(W, np.minimum(c0 + B, W) + d) - np.maximum(0, c0 - d)
+    return M, N
+
+
+def canonical_fold(picks, F1, F2):
+    """Vectorised reference canonical folding (tests/reference.py:59-71):
+    picks [n, I, 2] with per-block DFT sizes F1[n], F2[n] (or scalars)."""
+    a = picks[..., 0].astype(np.int64)
+    b = picks[..., 1].astype(np.int64)
+    F1 = np.broadcast_to(np.asarray(F1, dtype=np.int64).reshape(-1, 1), a.shape)
+    F2 = np.broadcast_to(np.asarray(F2, dtype=np.int64).reshape(-1, 1), a.shape)
+    ta, tb = (F1 - a) % F1, (F2 - b) % F2
+    twin = (ta < a) | ((ta == a) & (tb < b))
+    return np.stack([np.where(twin, ta, a), np.where(twin, tb, b)], axis=-1)
+
+
+def pick_hash(canon):
+    """64-bit FNV-1a over each row's (a, b) pairs, vectorised over rows
+    (the hash make_golden_large.py stores)."""
+    canon = np.asarray(canon, dtype=np.int64).reshape(len(canon), -1)
+    h = np.full(len(canon), 0xCBF29CE484222325, dtype=np.uint64)
+    prime = np.uint64(0x100000001B3)
+    for k in range(canon.shape[1]):
+        h ^= (canon[:, k] & 0xFFFF).astype(np.uint64)
+        h *= prime
+    return h.view(np.int64)

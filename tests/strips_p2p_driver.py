@@ -25,6 +25,47 @@ def worker(rank, world, port, cfg, B, crop, q):
         t = time.perf_counter()
         out = strips.conceal_strips(img, mask, p, prec, transport=tr)
         res.setdefault((tr, prec), []).append((out, time.perf_counter() - t))
+    # one PeerLink reused over runs whose level counts shrink (flag bases must
+    # keep increasing: ADVICE r1), frame buffer fixed as in bench.py
+    H, W = mask.shape
+    work = torch.empty((H, W), dtype=torch.float64, device="cuda")
+    msk = torch.from_numpy(mask).cuda()
+    mout = torch.empty_like(msk)
+    link = strips.open_peer_link(work, rank, world, dist)
+    R = strips.halo_rows(p)
+    reuse = []
+    masks = [mask]
+    m2 = mask.copy()
+    m2[:, W // 2:] = 0  # half the losses: fewer levels
+    masks.append(m2)
+    for mk in masks + masks[:1]:
+        plan = P.build_plan(mk, p)
+        processed = (plan.ranks() != np.iinfo(np.int32).max).reshape(plan.rows, plan.cols)
+        bands = strips.band_partition(processed.sum(axis=1), world, R)
+        work.copy_(torch.from_numpy(img.astype(np.float64)))
+        msk.copy_(torch.from_numpy(mk))
+        ex = strips.ShardExecutor(plan, bands[rank], work, msk, mout, p, "fp64")
+        fused = link is not None and strips.run_levels_p2p(ex, link, dist)
+        if not fused:
+            strips.run_levels_collective(ex, work, rank, world, bands, R, B, H, dist)
+        ex.close()
+        torch.cuda.synchronize()
+        dist.barrier()
+        lo, hi = bands[rank]
+        y0, y1 = lo * B, min(H, hi * B)
+        rows = work[y0:y1].cpu()
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (y0, y1, rows.numpy()))
+        full = np.zeros((H, W))
+        for a0, a1, r in gathered:
+            full[a0:a1] = r
+        reuse.append((mk, full, fused, plan.n_levels))
+    if link is not None:
+        link.close()
+    # default FseParams DFT size (fft_size=None): the fused exchange is not
+    # available, every rank must fall back to the collective one together
+    pn = P.FseParams(d=14, iterations=20, block_size=B)
+    outn = strips.conceal_strips(img, mask, pn, "fp64", transport="p2p")
     if rank == 0:
         ok = {}
         for prec in ("fp32", "fp64"):
@@ -32,6 +73,12 @@ def worker(rank, world, port, cfg, B, crop, q):
             for (tr, pr), runs in res.items():
                 if pr == prec:
                     ok[f"{tr}-{pr}"] = all(np.array_equal(o[0], whole) and np.array_equal(o[1], wm) for o, _ in runs)
+        for i, (mk, full, fused, nl) in enumerate(reuse):
+            whole, _, _ = P.conceal(img, mk, p, precision="fp64")
+            ok[f"reuse{i}-fused{int(fused)}-levels{nl}"] = bool(np.array_equal(full, whole)) and (
+                fused or link is None)
+        wn, wnm, _ = P.conceal(img, mask, pn, precision="fp64")
+        ok["fft_none_fallback"] = bool(np.array_equal(outn[0], wn) and np.array_equal(outn[1], wnm))
         q.put(ok)
     dist.barrier()
     dist.destroy_process_group()

@@ -570,3 +570,67 @@ def test_conceal_stream_equals_per_frame(prec, batch, depth):
         one, om, _ = P.conceal(frames[f], masks[f], p, precision=prec)
         assert got[f][0].astype(np.float64).tobytes() == one.tobytes()
         np.testing.assert_array_equal(got[f][1], om)
+
+
+# ---- full-size reference goldens (tests/golden/make_golden_large.py) ----------
+
+LARGE = ["cfg3", "cfg4f0", "cfg5crop", "cfg3def"]
+
+
+@pytest.mark.parametrize("name", LARGE)
+def test_large_golden_fp64_identical_picks(golden, name):
+    """BASELINE config 3, config 4 frame 0, a 768x1024 crop of the 4K config-5
+    frame, and config 3 with the reference's DEFAULT parameters (the drop-in
+    call, DFT = window size): fp64 canonical pick sequence of EVERY block
+    identical to the reference's (64-bit hash of each sequence, full sequences
+    of every 16th block), every lost sample within 1e-6, batches and mask equal."""
+    from helpers import canonical_fold, large_case, pick_hash, window_shapes
+
+    g = golden(f"large_{name}.npz")
+    img, mask, kw, fft = large_case(g)
+    p = P.FseParams(fft_size=fft, **kw)
+    out, msk, rep, picks = P.conceal(img, mask, p, "optimized", precision="fp64", return_picks=True)
+    assert rep.batches == csr(g["batch_ptr"], g["batch_blocks"])
+    assert rep.unconcealed_blocks == g["unconcealed"].tolist()
+    assert int(msk.astype(np.int64).sum()) == int(g["out_mask_sum"])
+    lost = mask == 1
+    err = np.abs(out[lost] - g["lost_values"])
+    assert float(err.max()) <= 1e-6, (float(err.max()), int((err > 1e-6).sum()))
+    blocks = g["pick_blocks"]
+    H, W = mask.shape
+    if fft is None:
+        F1, F2 = window_shapes(H, W, kw["block_size"], kw["d"], blocks)
+    else:
+        F1, F2 = fft
+    canon = canonical_fold(picks[blocks], F1, F2)
+    bad = np.flatnonzero(pick_hash(canon) != g["pick_hash"])
+    assert bad.size == 0, f"{bad.size} blocks differ, first {blocks[bad[:5]].tolist()}"
+    idx = np.searchsorted(blocks, g["sample_blocks"])
+    np.testing.assert_array_equal(canon[idx], g["sample_picks"].astype(np.int64))
+
+
+def test_conceal_batch_64_frames_fp64_matches_reference_frame0(golden):
+    """The bench path (conceal_batch over BASELINE config 4's 64 frames, every
+    frame's level in one merged launch, staged chunks) in fp64: frame 0 equals
+    the reference's frame 0 within 1e-6; every frame equals per-frame conceal()
+    for a sample of frames."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from helpers import large_case
+
+    g = golden("large_cfg4f0.npz")
+    img0, mask0, kw, fft = large_case(g)
+    with ThreadPoolExecutor(8) as ex:
+        scenes = list(ex.map(lambda f: synth.config_scene(4, f), range(64)))
+    imgs = np.stack([s[0] for s in scenes])
+    msks = np.stack([s[1] for s in scenes])
+    assert np.array_equal(imgs[0], img0) and np.array_equal(msks[0], mask0)
+    p = P.FseParams(fft_size=fft, **kw)
+    out, om, _ = P.conceal_batch(imgs, msks, p, "optimized", "fp64", reports=False)
+    lost = mask0 == 1
+    assert float(np.max(np.abs(out[0][lost] - g["lost_values"]))) <= 1e-6
+    assert int(om[0].astype(np.int64).sum()) == int(g["out_mask_sum"])
+    for f in (1, 31, 63):
+        o1, m1, _ = P.conceal(imgs[f], msks[f], p, "optimized", precision="fp64")
+        np.testing.assert_array_equal(out[f], o1)
+        np.testing.assert_array_equal(om[f], m1)

@@ -112,6 +112,32 @@ def test_small_grids_and_empty():
     assert c[12] == 0 and all(v == -1 for i, v in enumerate(c) if i != 12)
 
 
+def test_caller_counts_below_zero_become_done():
+    """schedule.py:85-94 on counts a caller supplies: a pending block whose count
+    a commit drops below 0 is never selected (the reference returns [[0]] here)."""
+    g = grid_of(1, 2)
+    assert P.schedule_all(g, np.array([0, 0], np.int32)) == [[0]]
+    g3 = grid_of(3, 3)
+    c = np.zeros(9, np.int32)
+    assert P.schedule_all(g3, c) == O.schedule_all(O.Grid.of(12, 12, 4), c)
+
+
+@settings(max_examples=60, deadline=None)
+@given(rows=st.integers(1, 8), cols=st.integers(1, 8), seed=st.integers(0, 2**31 - 1))
+def test_schedule_arbitrary_counts_match_restatement(rows, cols, seed):
+    """Any int counts (including 0s next to each other, large values and -1s)
+    give the reference's batch sequence (oracle restatement of schedule.py)."""
+    rng = np.random.default_rng(seed)
+    c = rng.integers(-2, 40, size=rows * cols).astype(np.int32)
+    c[rng.uniform(size=c.size) < 0.2] = 0
+    assert P.schedule_all(grid_of(rows, cols), c) == O.schedule_all(O.Grid.of(rows * 4, cols * 4, 4), c)
+
+
+def test_schedule_rejects_huge_counts():
+    with pytest.raises(Exception):
+        P.schedule_all(grid_of(2, 2), np.array([0, 1 << 20, 1, 2], np.int32))
+
+
 @settings(max_examples=40, deadline=None)
 @given(rows=st.integers(1, 9), cols=st.integers(1, 9), seed=st.integers(0, 2**31 - 1),
        density=st.floats(0.05, 1.0))
@@ -301,3 +327,19 @@ def test_abi_argument_errors_without_a_device():
     assert L.fse_set_track_below(-1) == _lib.FSE_EINVAL
     assert b"track_below" in L.fse_last_error()
     assert L.fse_shard_run(None, 0, 1, None) == _lib.FSE_EINVAL
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg4f0", "cfg5crop", "cfg3def"])
+def test_large_golden_batches_from_cpp_planner(golden, name):
+    """The C++ planner's batches on full-size frames equal the reference's
+    (tests/golden/make_golden_large.py), and the fixture's sampled full pick
+    sequences agree with its per-block hashes."""
+    from helpers import large_case, pick_hash
+
+    g = golden(f"large_{name}.npz")
+    img, mask, kw, fft = large_case(g)
+    plan = P.build_plan(mask, P.FseParams(fft_size=fft, **kw))
+    assert plan.batches() == csr(g["batch_ptr"], g["batch_blocks"])
+    assert plan.unconcealed() == g["unconcealed"].tolist()
+    idx = np.searchsorted(g["pick_blocks"], g["sample_blocks"])
+    np.testing.assert_array_equal(pick_hash(g["sample_picks"]), g["pick_hash"][idx])
