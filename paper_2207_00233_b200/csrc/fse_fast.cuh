@@ -244,6 +244,33 @@ __device__ __forceinline__ void warp_argmax(unsigned long long key, unsigned lin
     wlin = warp_min_u32(hi == mh && lo == ml ? lin : 0xFFFFFFFFu);
 }
 
+// Warp argmax of (key, lin) as above, returning the lane that holds it (the
+// lowest lane among equals) instead of the key: the common case -- one lane
+// holds the largest key, or for 64-bit keys the largest high word -- costs one
+// REDUX and one ballot; only ties in that first REDUX take the full
+// (key, lin) reduction.  Keys are per-lane best-of-bins with strict '>' in
+// row-major bin order, so a unique holder's lin is already the first maximum.
+__device__ __forceinline__ int warp_argmax_lane(unsigned key, unsigned lin) {
+    const unsigned mk = warp_max_u32(key);
+    unsigned cand = __ballot_sync(0xffffffffu, key == mk);
+    if (__popc(cand) > 1) {
+        const unsigned ml = warp_min_u32(key == mk ? lin : 0xFFFFFFFFu);
+        cand = __ballot_sync(0xffffffffu, key == mk && lin == ml);
+    }
+    return __ffs(cand) - 1;
+}
+__device__ __forceinline__ int warp_argmax_lane(unsigned long long key, unsigned lin) {
+    const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+    const unsigned mh = warp_max_u32(hi);
+    unsigned cand = __ballot_sync(0xffffffffu, hi == mh);
+    if (__popc(cand) > 1) {
+        const unsigned ml = warp_max_u32(hi == mh ? lo : 0u);
+        const unsigned mi = warp_min_u32(hi == mh && lo == ml ? lin : 0xFFFFFFFFu);
+        cand = __ballot_sync(0xffffffffu, hi == mh && lo == ml && lin == mi);
+    }
+    return __ffs(cand) - 1;
+}
+
 // ---- complex pair arithmetic.  fp32 uses the sm_100 packed f32x2 pipe
 // (FADD2 / FFMA2: two lanes of fp32 math per instruction, with scalar
 // broadcast and half-swizzle operands), halving the issue slots of the
@@ -541,7 +568,13 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
 #pragma unroll
     for (int i = 0; i < NR; ++i) twr[i] = tw[(v0 * q4 + tstep * i) & (F - 1)];
     auto partials = [&](const T2 *Y) {
+        // (-DFSE_PART_NOUNROLL halves the kernel's code: config 1 fp64 1.9 vs
+        // 2.0 ms, but config 4 fp32 +6%, fp64 +0.5%: unrolled by default)
+#ifdef FSE_PART_NOUNROLL
+#pragma unroll 1
+#else
 #pragma unroll
+#endif
         for (int j = 0; j < NB; ++j) {
             const int u = u0 + RSTEP * j;
             if (u < R1) {
@@ -647,8 +680,15 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     }
     __syncthreads();
 
+    // sum(w) (_kernel.pyx:144): fp64 takes W[0][0] = sum_mn w[m][n] e^0, which
+    // the DFT passes form in an order fixed by F and the window alone, so every
+    // variant of one F (warps per window, executor) divides by the same bits;
+    // the staging sum above depends on the warp count.  fp32 rounds the
+    // double staging sum to float.
+    double total_used = total;
+    if constexpr (!IS_F32) total_used = (double)Wext[C::EXT ? (F / 2) * F : 0].x;
     const T gamma = (T)A.gamma;
-    const T tot = (T)total;
+    const T tot = (T)total_used;
     const T inv_tot = (T)1 / tot;
     const int I = A.iterations;
     int32_t *picks_out = nullptr;
@@ -679,8 +719,29 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     constexpr bool LAZY = IS_F32 && CL == 1 && !GUARD && !C::TRACK;
     T tmax = (T)0;
     using KeyT = decltype(energy_key((T)0));
+    // LAZY64 (fp64): the running maximum of the energies' HIGH words only --
+    // one integer max per bin instead of a compare and seven moves.  The high
+    // word of a double >= 0 orders like the value to 20 mantissa bits, so the
+    // CTA maximum H of the high words selects the candidate bins (high word
+    // == H, i.e. within ~1e-6 relative of the maximum); the lanes holding
+    // them recompute those energies exactly and resolve the argmax on the full
+    // 64-bit keys, ties to the smallest row-major index, after a second
+    // barrier -- the same first maximum as the strict '>' scan of
+    // _kernel.pyx:32-44.  (Non-finite energies, i.e. NaN/inf inputs, and
+    // energies below 2^-1002 are outside this contract.)
+    // Measured slower than the tracked one-barrier argmax (config 4 fp64
+    // 564.6 vs 545.5 ms, config 1 2.1 vs 1.9 ms: the second barrier costs more
+    // than the moves it saves), so opt-in only (-DFSE_LAZY64).
+#ifdef FSE_LAZY64
+    constexpr bool LAZY64 = !IS_F32 && CL == 1 && !GUARD && !C::TRACK;
+#else
+    constexpr bool LAZY64 = false;
+#endif
+    unsigned hmax = 0;
     auto track = [&](int j, T e) {
-        if constexpr (LAZY) {
+        if constexpr (LAZY64) {
+            hmax = max(hmax, (unsigned)__double2hiint((double)e));
+        } else if constexpr (LAZY) {
             tmax = fmax(tmax, e);  // NaN never wins, like the strict '>' scan
         } else if constexpr (IS_F32 && GUARD) {
             const unsigned key = (__float_as_uint((float)e) & ~0x1Fu) | (unsigned)(31 - j);
@@ -713,7 +774,12 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         KeyT *ska = reinterpret_cast<KeyT *>(reinterpret_cast<unsigned long long *>(slots) + (it & 1) * NWT);
         ArgSlot<T> *skb = reinterpret_cast<ArgSlot<T> *>(reinterpret_cast<unsigned long long *>(slots) + 2 * NWT);
         KeyT wk = 0;
-        if constexpr (LAZY) {
+        unsigned *ska32 = reinterpret_cast<unsigned *>(reinterpret_cast<unsigned long long *>(slots) + (it & 1) * NWT);
+        unsigned wk32 = 0;
+        if constexpr (LAZY64) {
+            wk32 = warp_max_u32(hmax);
+            if (lane == 0) ska32[warp] = wk32;
+        } else if constexpr (LAZY) {
             wk = warp_max_k(energy_key(tmax));
             if (lane == 0) ska[warp] = wk;
         } else if constexpr (IS_F32 && GUARD) {
@@ -730,15 +796,22 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
             }
         } else {
             const auto key = energy_key(best);
+            // one writer: the lane of the warp's first maximum (when the warp
+            // has no bin above 0, every lane holds the same empty slot)
+#ifndef FSE_ARGMAX_FULL
+            if (lane == warp_argmax_lane(key, blin)) {
+                ArgSlot<T> mine;
+                mine.key = key;
+                mine.lin = blin;
+#else
             decltype(energy_key(best)) wkey;
             unsigned wlin;
             warp_argmax(key, blin, wkey, wlin);
-            // one writer: the lane of the warp's first maximum (all lanes when
-            // the warp has no bin above 0; they all hold the same empty slot)
             if (key == wkey && blin == wlin) {
                 ArgSlot<T> mine;
                 mine.key = wkey;
                 mine.lin = wlin;
+#endif
                 mine.gre = bg.x;
                 mine.gim = bg.y;
                 if constexpr (CL > 1) {  // into the slot array of every CTA of the cluster
@@ -754,7 +827,59 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         else __syncthreads();
         int a, b;
         T2 gwin;
-        if constexpr (LAZY) {
+        if constexpr (LAZY64) {
+            const bool in = lane < NWT;
+            const unsigned uk = in ? ska32[lane] : 0u;
+            const unsigned H = warp_max_u32(uk);
+            if (H == 0) {
+                // no energy above 2^-1002 (an all-zero window): the strict '>'
+                // scan from -1 keeps (0, 0) (_kernel.pyx:32-44), g = 0
+                a = b = 0;
+                gwin = T2{0, 0};
+            } else {
+                if (wk32 == H) {
+                    // a candidate warp: its lanes at H resolve their bins with
+                    // high word H on the exact keys (first maximum in row-major order)
+                    unsigned long long bkey = 0;
+                    unsigned mylin = 0xFFFFFFFFu;
+                    T2 myg = T2{0, 0};
+                    if (hmax == H) {
+#pragma unroll
+                        for (int j = 0; j < NB; ++j) {
+                            const bool inr = (j < NB - 1) || (C::NSEGS % NWT == 0) || (u0 + RSTEP * j < R1);
+                            const bool ok = (j == 0 || j == NB - 1) ? ((valid >> j) & 1u) != 0 : inr;
+                            const T e = energy(G[j]);
+                            const unsigned long long k = energy_key(e);
+                            if (ok && (unsigned)(k >> 32) == H && k > bkey) {
+                                bkey = k;
+                                mylin = lin0 + (unsigned)(j * RSTEP * F);
+                                myg = G[j];
+                            }
+                        }
+                    }
+                    const unsigned hb = __ballot_sync(0xffffffffu, hmax == H);
+                    const int wl = __popc(hb) == 1 ? __ffs(hb) - 1 : warp_argmax_lane(bkey, mylin);
+                    if (lane == wl) {
+                        ArgSlot<T> mine;
+                        mine.key = bkey;
+                        mine.lin = mylin;
+                        mine.gre = myg.x;
+                        mine.gim = myg.y;
+                        skb[warp] = mine;
+                    }
+                }
+                __syncthreads();
+                const bool cand = in && uk == H;
+                const unsigned cb = __ballot_sync(0xffffffffu, cand);
+                const int gw = __popc(cb) == 1
+                                   ? __ffs(cb) - 1
+                                   : warp_argmax_lane(cand ? skb[lane].key : 0ull, cand ? skb[lane].lin : 0xFFFFFFFFu);
+                const unsigned glin = skb[gw].lin;
+                a = (int)(glin / F);
+                b = (int)(glin & (F - 1));
+                gwin = T2{skb[gw].gre, skb[gw].gim};
+            }
+        } else if constexpr (LAZY) {
             const bool in = lane < NWT;
             const KeyT uk = in ? ska[lane] : (KeyT)0;
             const KeyT gk = warp_max_k(uk);
@@ -780,7 +905,14 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
                             }
                         }
                     }
+#ifndef FSE_ARGMAX_FULL
+                    // usually one lane of the warp is at the maximum: no REDUX
+                    const unsigned hb = __ballot_sync(0xffffffffu, mylin != 0xFFFFFFFFu);
+                    const unsigned wl = __popc(hb) == 1 ? __shfl_sync(0xffffffffu, mylin, __ffs(hb) - 1)
+                                                        : warp_min_u32(mylin);
+#else
                     const unsigned wl = warp_min_u32(mylin);
+#endif
                     if (mylin == wl) {
                         ArgSlot<T> mine;
                         mine.key = gk;
@@ -793,7 +925,14 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
                 __syncthreads();
                 const bool cand = in && uk == gk;
                 const unsigned ul = cand ? skb[lane].lin : 0xFFFFFFFFu;
+#ifndef FSE_ARGMAX_FULL
+                // usually one warp holds the maximum: no REDUX
+                const unsigned cb = __ballot_sync(0xffffffffu, cand);
+                const unsigned glin = __popc(cb) == 1 ? __shfl_sync(0xffffffffu, ul, __ffs(cb) - 1)
+                                                      : warp_min_u32(ul);
+#else
                 const unsigned glin = warp_min_u32(ul);
+#endif
                 const int gw = __ffs(__ballot_sync(0xffffffffu, cand && ul == glin)) - 1;
                 a = (int)(glin / F);
                 b = (int)(glin & (F - 1));
@@ -828,11 +967,18 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
             const bool in = lane < NWT;
             const auto uk = in ? asl[lane].key : decltype(asl[0].key)(0);
             const unsigned ul = in ? asl[lane].lin : 0xFFFFFFFFu;
+#ifndef FSE_ARGMAX_FULL
+            // the winning slot (when no bin is above 0 every slot holds g = 0
+            // and lin = none, and the lowest slot wins)
+            const int gw = warp_argmax_lane(uk, ul);
+            unsigned glin = __shfl_sync(0xffffffffu, ul, gw);
+#else
             decltype(asl[0].key) gk;
             unsigned glin;
             warp_argmax(uk, ul, gk, glin);
             // the winning slot (any slot when no bin is above 0: all hold g = 0)
             const int gw = __ffs(__ballot_sync(0xffffffffu, in && ul == glin)) - 1;
+#endif
             // no bin above 0 (all energies 0 or NaN): the reference's strict-'>'
             // scan from -1 keeps (0, 0) (_kernel.pyx:32-44), whose g is 0
             if (glin >= (unsigned)(R1 * F)) glin = 0;
@@ -890,6 +1036,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         best = (T)0;
         blin = 0xFFFFFFFFu;
         tmax = (T)0;
+        hmax = 0;
         const T2 mS = T2{-gpr, -gpr}, qv = T2{gpi, -gpi};
         // loads of a group of LG bins are issued before its math (smem latency);
         // measured on config 4: fp32 LG 1/2/3/4/6/11 = 284.2/283.4/289.2/287.5/

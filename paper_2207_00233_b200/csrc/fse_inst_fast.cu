@@ -80,6 +80,18 @@ using Fast64T = FastCfg<float, 64, 6, true, 4, 1, true>;
 // (config 3: 19.8 vs 23.3 ms; 22 warps: slower everywhere)
 using Fast64L = FastCfg<float, 64, 12, true, 2, 1, true>;
 using Fast32T = FastCfg<float, 32, FSE_F32_32_NW, true, FSE_F32_32_MINB, 1, true>;
+// fp64 levels of at most one window per SM (configs 1 and 2, narrow levels of
+// 3 and 5) with more warps per window (dev knob FSE_F64L = 12 / 22; default 0
+// = the 6-warp kernel: measured config 1 2.1 / 2.2 / 2.1 ms for 12 / 22 / 6)
+using Fast64D12 = FastCfg<double, 64, 12, false, 1>;
+using Fast64D22 = FastCfg<double, 64, 22, false, 1>;
+static int f64_narrow_warps() {
+    static const int v = [] {
+        const char *e = getenv("FSE_F64L");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
 
 // Levels narrower than this many windows use the tracked argmax (fp32):
 // measured on configs 2 (linescan), 3 and 5 -- levels of a few hundred
@@ -256,7 +268,11 @@ int fast_level(int dtype, int F, bool guard, const FastArgs &a, int grid, int Mm
         return narrow ? launch<Fast32T, 0, false>(a, grid, Mmax, Nmax, model_n, s)
                       : launch<Fast32<float>, 0, false>(a, grid, Mmax, Nmax, model_n, s);
     }
-    if (F == 64) return launch<Fast64<double>, 0, false>(a, grid, Mmax, Nmax, model_n, s);
+    if (F == 64) {
+        if (grid <= sms && f64_narrow_warps() == 12) return launch<Fast64D12, 0, false>(a, grid, Mmax, Nmax, model_n, s);
+        if (grid <= sms && f64_narrow_warps() == 22) return launch<Fast64D22, 0, false>(a, grid, Mmax, Nmax, model_n, s);
+        return launch<Fast64<double>, 0, false>(a, grid, Mmax, Nmax, model_n, s);
+    }
     return launch<Fast32<double>, 0, false>(a, grid, Mmax, Nmax, model_n, s);
 }
 

@@ -92,12 +92,16 @@ constexpr int kMaxCount = 1 << 14;
 // count value, scanned in row-major order for the current minimum.  Selection
 // of a whole batch happens before any commit, as in select_batch/commit_batch.
 
+template <typename CT>
+void schedule_loop(const int32_t *counts_in, int rows, int cols, int maxc, long pending,
+                   std::vector<int32_t> &ptr, std::vector<int32_t> &blocks);
+
 int schedule_impl(const int32_t *counts_in, int rows, int cols,
                   std::vector<int32_t> &ptr, std::vector<int32_t> &blocks) {
     const int nb = rows * cols;
-    const int words = (nb + 63) / 64;
-    // Pending counts (>= 0) fit in int16; everything below 0 is done and its
-    // exact value never matters again (select_batch only looks at counts >= 0,
+    // Pending counts (>= 0) fit in int8 for init_counts' counts (<= 13) and in
+    // int16 up to kMaxCount; everything below 0 is done and its exact value
+    // never matters again (select_batch only looks at counts >= 0,
     // schedule.py:69-70), so done blocks are kept at -1 instead of drifting.
     int maxc = 0;
     long pending = 0;
@@ -109,8 +113,18 @@ int schedule_impl(const int32_t *counts_in, int rows, int cols,
             maxc = std::max(maxc, (int)counts_in[b]);
             ++pending;
         }
-    std::vector<int16_t> cnt(nb);
-    for (int b = 0; b < nb; ++b) cnt[b] = (int16_t)(counts_in[b] >= 0 ? counts_in[b] : -1);
+    if (maxc <= 126) schedule_loop<int8_t>(counts_in, rows, cols, maxc, pending, ptr, blocks);
+    else schedule_loop<int16_t>(counts_in, rows, cols, maxc, pending, ptr, blocks);
+    return FSE_OK;
+}
+
+template <typename CT>
+void schedule_loop(const int32_t *counts_in, int rows, int cols, int maxc, long pending,
+                   std::vector<int32_t> &ptr, std::vector<int32_t> &blocks) {
+    const int nb = rows * cols;
+    const int words = (nb + 63) / 64;
+    std::vector<CT> cnt(nb);
+    for (int b = 0; b < nb; ++b) cnt[b] = (CT)(counts_in[b] >= 0 ? counts_in[b] : -1);
     // bucket c: bitset of pending blocks with count c; summary: bitset of its
     // non-zero words, so a row-major scan skips empty stretches 64 words at a
     // time.  The count is the fast index of both arrays: a neighbour's move
@@ -213,7 +227,6 @@ int schedule_impl(const int32_t *counts_in, int rows, int cols,
         if (prof) t_com += ms(q1, now());
     }
     if (prof) fprintf(stderr, "plan   schedule loop: select %.1f ms, commit %.1f ms\n", t_sel, t_com);
-    return FSE_OK;
 }
 
 struct Geometry {

@@ -7,7 +7,7 @@ for rep in 1 2; do
     FSE_LIB=$lib python bench.py --steps 3 --warmup 2 --no-e2e --no-cpu-baseline $AB_ARGS > /tmp/ab.log 2>&1
     python -c "
 import json,sys;d=json.loads(open('/tmp/ab.log').read().strip().splitlines()[-1])
-s=d.get('fp64') or {}
-print('$v', round(d['kernel_ms_per_step'],2), round(d['roofline']['frac'],4), round(s.get('kernel_ms_per_step',0),2))" || tail -3 /tmp/ab.log
+s=d.get('fp64') or d.get('fp32') or {}
+print('$v', d['dtype'], round(d['kernel_ms_per_step'],2), round(d['roofline']['frac'],4), 'other', round(s.get('kernel_ms_per_step',0),2))" || tail -3 /tmp/ab.log
   done
 done
