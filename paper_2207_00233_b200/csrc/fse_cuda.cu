@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "fse_fast.cuh"
+#include "fse_gen.cuh"
 
 namespace fse {
 
@@ -265,6 +266,14 @@ int dispatch(const KArgs &a, int grid, int Mmax, int Nmax, int F1, int F2, int m
         if (F1 == 128) return launch_variant<CfgF128<T>, MODE, DEBUG>(a, grid, Mmax, Nmax, 128, 128, model_n, s);
     }
     const int F1m = F1 ? F1 : Mmax, F2m = F2 ? F2 : Nmax;
+    if constexpr (!DEBUG) {
+        // any-size kernel (fse_gen.cuh): W row-extended plane, canonical bins,
+        // tracked argmax; the older generic kernel below stays for the debug
+        // outputs (energies / residual) and sizes the new one does not fit
+        const int rc = gen_launch(std::is_same<T, double>::value ? FSE_F64 : FSE_F32, MODE, a, grid, Mmax, Nmax,
+                                  F1m, F2m, model_n, s);
+        if (rc != FSE_ENOTSUP) return rc;
+    }
     if ((F1m / 2 + 1) * F2m > CfgGen<T>::NB * CfgGen<T>::NT)
         return fail(FSE_ENOTSUP, "DFT size " + std::to_string(F1m) + "x" + std::to_string(F2m) +
                                      " exceeds the generic kernel's bin capacity");
