@@ -993,8 +993,18 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
             gpr = gwin.x * ginv;
             gpi = gwin.y * ginv;
         } else {
+#ifndef FSE_P_DIV
+            // gamma / sum(w) folded into one factor, as in fp32: p differs from
+            // the correctly rounded g / sum(w) of _kernel.pyx:46-47 by an ulp,
+            // far below any pick margin; the exact quotient (-DFSE_P_DIV) costs
+            // three dependent DFMA on every iteration's critical path
+            // (config 4: 551.6 -> 542.8 ms without it)
+            gpr = gwin.x * ginv;
+            gpi = gwin.y * ginv;
+#else
             gpr = gamma * div_by(gwin.x, tot, inv_tot);
             gpi = gamma * div_by(gwin.y, tot, inv_tot);
+#endif
         }
         if constexpr (MODE == 1) {
             if (gwarp == 0 && lane == 0) {

@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <atomic>
 #include <climits>
+#include <limits>
 #include <cstring>
 #include <thread>
 #include <chrono>
@@ -146,8 +147,10 @@ void schedule_loop(const int32_t *counts_in, int rows, int cols, int maxc, long 
     };
     for (int b = 0; b < nb; ++b)
         if (cnt[b] >= 0) add(cnt[b], b);
-    // blocks taken in the current phase (reset through the batch list)
-    std::vector<uint8_t> taken(nb, 0);
+    // blocks taken in the current phase are marked in the count array itself
+    // (kTaken, above every pending count; set to -1 by the commit), so the
+    // clash test reads the count lines the commit touches next anyway
+    const CT kTaken = std::numeric_limits<CT>::max();
     ptr.assign(1, 0);
     blocks.clear();
     blocks.reserve(pending);
@@ -173,14 +176,15 @@ void schedule_loop(const int32_t *counts_in, int rows, int cols, int maxc, long 
                     int r = b / cols, c = b - r * cols;
                     // only row-major-earlier neighbours can already be taken
                     bool clash = false;
-                    if (c > 0 && taken[b - 1]) clash = true;
+                    if (c > 0 && cnt[b - 1] == kTaken) clash = true;
                     if (!clash && r > 0) {
                         int up = b - cols;
-                        if (taken[up] || (c > 0 && taken[up - 1]) || (c + 1 < cols && taken[up + 1]))
+                        if (cnt[up] == kTaken || (c > 0 && cnt[up - 1] == kTaken) ||
+                            (c + 1 < cols && cnt[up + 1] == kTaken))
                             clash = true;
                     }
                     if (clash) continue;
-                    taken[b] = 1;
+                    cnt[b] = kTaken;
                     batch.push_back(b);
                 }
             }
@@ -190,7 +194,6 @@ void schedule_loop(const int32_t *counts_in, int rows, int cols, int maxc, long 
         for (int b : batch) {
             del(nmin, b);
             cnt[b] = -1;
-            taken[b] = 0;
             --pending;
         }
         // commit_batch (schedule.py:85-94): every neighbour's count drops by
