@@ -18,7 +18,7 @@ FSE_ORDER_OPTIMIZED, FSE_ORDER_LINESCAN = 0, 1
 FSE_IPC_HANDLE_BYTES = 72
 
 EXPORTS = (
-    "fse_last_error", "fse_version", "fse_run_windows", "fse_plan_build", "fse_plan_build_many",
+    "fse_last_error", "fse_version", "fse_run_windows", "fse_plan_build", "fse_plan_build_threads", "fse_plan_build_many",
     "fse_plan_free", "fse_plan_sizes", "fse_plan_batches", "fse_plan_levels", "fse_plan_ranks",
     "fse_plan_unconcealed", "fse_init_counts", "fse_schedule_all", "fse_conceal_frames",
     "fse_launch_count", "fse_timing_enable", "fse_timing_read", "fse_fma_probe",
@@ -62,6 +62,12 @@ def lib():
                 f"{LIB_PATH} is not built; run `python -m paper_2207_00233_b200.build` "
                 "(there is no CPU fallback)"
             )
+        # one process per GPU (torchrun): the host planner's threads
+        # (fse_plan_build, automatic count) share the node's CPUs among the
+        # local ranks instead of each rank taking all of them
+        lws = int(os.environ.get("LOCAL_WORLD_SIZE", "1") or 1)
+        if lws > 1 and "FSE_PLAN_THREADS" not in os.environ:
+            os.environ["FSE_PLAN_THREADS"] = str(max(1, len(os.sched_getaffinity(0)) // lws))
         L = ctypes.CDLL(LIB_PATH)
         L.fse_last_error.restype = ctypes.c_char_p
         L.fse_version.argtypes = [_pi32, _i32]
@@ -69,6 +75,8 @@ def lib():
                                       _i32, _vp, _vp, _vp, _vp, _vp]
         L.fse_plan_build.argtypes = [_vp, _i32, _i32, ctypes.POINTER(FseParamsC), _i32,
                                      ctypes.POINTER(_vp)]
+        L.fse_plan_build_threads.argtypes = [_vp, _i32, _i32, ctypes.POINTER(FseParamsC), _i32, _i32,
+                                             ctypes.POINTER(_vp)]
         L.fse_plan_build_many.argtypes = [_i32, ctypes.POINTER(_vp), _i32, _i32,
                                           ctypes.POINTER(FseParamsC), _i32, _i32, ctypes.POINTER(_vp)]
         L.fse_plan_free.argtypes = [_vp]

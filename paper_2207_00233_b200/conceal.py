@@ -94,12 +94,14 @@ def _order_code(order: str) -> int:
     return _lib.FSE_ORDER_LINESCAN if order == LINESCAN else _lib.FSE_ORDER_OPTIMIZED
 
 
-def build_plan(mask: np.ndarray, params: FseParams, order: str = OPTIMIZED) -> Plan:
+def build_plan(mask: np.ndarray, params: FseParams, order: str = OPTIMIZED, plan_threads: int = 0) -> Plan:
+    """Host plan of one frame (fse_plan_build_threads; 0 = automatic thread count,
+    1 = the sequential planner -- the plan is identical either way)."""
     m = np.ascontiguousarray(mask, dtype=np.uint8)
     h = ctypes.c_void_p()
     pc = params.to_c()
-    _lib.check(_lib.lib().fse_plan_build(m.ctypes.data, m.shape[0], m.shape[1], ctypes.byref(pc),
-                                         _order_code(order), ctypes.byref(h)))
+    _lib.check(_lib.lib().fse_plan_build_threads(m.ctypes.data, m.shape[0], m.shape[1], ctypes.byref(pc),
+                                                 _order_code(order), int(plan_threads), ctypes.byref(h)))
     return Plan(h.value)
 
 

@@ -25,6 +25,9 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#ifdef __linux__
+#include <sched.h>
+#endif
 
 #include "fse_common.h"
 
@@ -286,133 +289,62 @@ int level_pass(const Plan &P, int rows, int cols, int R, std::vector<int32_t> &l
     return n_levels;
 }
 
-int build_one(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p, int32_t order,
-              Plan &P) {
-    int rc = validate(p, H, W, order);
-    if (rc) return rc;
-    Geometry G{H, W, p->block_size, (H + p->block_size - 1) / p->block_size,
-               (W + p->block_size - 1) / p->block_size, p->d};
-    const int rows = G.rows, cols = G.cols, nb = rows * cols, B = G.B;
-    P.H = H; P.W = W; P.B = B; P.rows = rows; P.cols = cols; P.d = p->d; P.order = order;
-    P.iterations = p->iterations; P.fft1 = p->fft1; P.fft2 = p->fft2;
-    P.rho = p->rho; P.delta = p->delta; P.gamma = p->gamma;
+// ---- host threads -------------------------------------------------------------
 
-    const bool prof = getenv("FSE_PLAN_TIMING") != nullptr;
-    auto clk = [] { return std::chrono::steady_clock::now(); };
-    auto t_start = clk();
-    auto lap = [&](const char *what) {
-        if (!prof) return;
-        auto now = clk();
-        fprintf(stderr, "plan %-12s %.1f ms\n", what, std::chrono::duration<double, std::milli>(now - t_start).count());
-        t_start = now;
-    };
-    // per-block presence flags (only "any" is ever needed): bit 0 a LOST sample
-    // (lost_per_block > 0, grid.py:138-144), bit 1 a RECONSTRUCTED sample, bit 2
-    // any other state (class A, grid.py:124-130).  Rows are scanned 8 bytes at a
-    // time; all-KNOWN and all-LOST words (the common cases) set one bit of
-    // their blocks without a per-byte pass.
-    std::vector<uint8_t> flag(nb, 0);
-    {
-        uint8_t lut[256];
-        for (int v = 0; v < 256; ++v) lut[v] = v == FSE_LOST ? 1 : (v == FSE_RECONSTRUCTED ? 2 : 4);
-        for (int y = 0; y < H; ++y) {
-            const uint8_t *row = mask + (size_t)y * W;
-            uint8_t *fr = &flag[(size_t)(y / B) * cols];
-            int x = 0;
-            for (; x + 8 <= W; x += 8) {
-                uint64_t w8;
-                std::memcpy(&w8, row + x, 8);
-                if (w8 == 0) {
-                    for (int c = x / B; c <= (x + 7) / B; ++c) fr[c] |= 4;
-                } else if (w8 == 0x0101010101010101ull) {  // a run of LOST samples
-                    for (int c = x / B; c <= (x + 7) / B; ++c) fr[c] |= 1;
-                } else {
-                    for (int i = 0; i < 8; ++i) fr[(x + i) / B] |= lut[row[x + i]];
-                }
-            }
-            for (; x < W; ++x) fr[x / B] |= lut[row[x]];
-        }
-    }
-    auto nL = [&](int b) { return (flag[b] & 1) != 0; };
-    auto nR0 = [&](int b) { return (flag[b] & 2) != 0; };
-    auto nA = [&](int b) { return (flag[b] & 4) != 0; };
-    std::vector<uint8_t> lossy(nb);
-    P.n_lossy = 0;
-    for (int b = 0; b < nb; ++b) {
-        lossy[b] = nL(b);
-        P.n_lossy += lossy[b];
-    }
-    P.max_wr = std::min(H, B + 2 * p->d);
-    P.max_wc = std::min(W, B + 2 * p->d);
+// Run fn(k) on threads k = 0..T-1 (k = 0 on the caller).
+template <class Fn>
+void run_threads(int T, Fn &&fn) {
+    std::vector<std::thread> pool;
+    pool.reserve(T > 1 ? T - 1 : 0);
+    for (int k = 1; k < T; ++k) pool.emplace_back([&fn, k] { fn(k); });
+    fn(0);
+    for (auto &t : pool) t.join();
+}
 
-    lap("tallies");
-    // processing phases in reference order
-    std::vector<int32_t> ph_ptr, ph_blocks;
-    if (order == FSE_ORDER_OPTIMIZED) {
-        std::vector<int32_t> counts(nb);
-        init_counts_impl(lossy.data(), rows, cols, counts.data());
-        lap("init_counts");
-        rc = schedule_impl(counts.data(), rows, cols, ph_ptr, ph_blocks);
-        if (rc) return rc;
-    } else {
-        ph_ptr.assign(1, 0);
-        for (int b = 0; b < nb; ++b)
-            if (lossy[b]) {
-                ph_blocks.push_back(b);
-                ph_ptr.push_back((int32_t)ph_blocks.size());
-            }
-    }
+int usable_cpus() {
+#ifdef __linux__
+    cpu_set_t set;
+    if (sched_getaffinity(0, sizeof(set), &set) == 0) return std::max(1, (int)CPU_COUNT(&set));
+#endif
+    return std::max(1, (int)std::thread::hardware_concurrency());
+}
 
-    lap("schedule");
-    // degeneracy (fse.py:150-151): no sample of positive weight.  A samples
-    // always weigh rho^dist > 0; R samples weigh delta*rho^dist, > 0 iff delta > 0.
-    std::vector<uint8_t> written(nb, 0);
-    const bool r_counts = p->delta > 0.0;
-    // Fast path: a block lying wholly inside the window that holds an A sample
-    // (or, with delta > 0, a pre-reconstructed sample) makes the window usable
-    // whatever was written since.  The fully covered block range of block
-    // (r, c)'s window is [ilo(r), ihi(r)] x [jlo(c), jhi(c)], both monotone in
-    // their argument, so one row-major sweep with vertical running counts per
-    // column and a prefix count along the row answers every block in O(1).
-    std::vector<uint8_t> sok(nb, 0);
-    {
-        auto lo_hi = [&](int i, int n, int S, int &lo, int &hi) {  // block i of n along an axis of S samples
-            const int s0 = std::max(0, i * B - p->d);
-            const int s1 = std::min(S, std::min(i * B + B, S) + p->d);
-            lo = (s0 + B - 1) / B;
-            hi = s1 == S ? n - 1 : s1 / B - 1;
-        };
-        std::vector<int> jlo(cols), jhi(cols);
-        for (int c = 0; c < cols; ++c) lo_hi(c, cols, W, jlo[c], jhi[c]);
-        std::vector<int32_t> vcnt(cols, 0), pre(cols + 1, 0);
-        int cur_lo = 0, cur_hi = -1;  // block rows summed into vcnt
-        for (int r = 0; r < rows; ++r) {
-            int ilo, ihi;
-            lo_hi(r, rows, H, ilo, ihi);
-            if (ilo > ihi) continue;
-            while (cur_hi < ihi) {
-                ++cur_hi;
-                for (int c = 0; c < cols; ++c) {
-                    const int o = cur_hi * cols + c;
-                    vcnt[c] += (nA(o) || (r_counts && nR0(o))) ? 1 : 0;
-                }
-            }
-            while (cur_lo < ilo) {
-                for (int c = 0; c < cols; ++c) {
-                    const int o = cur_lo * cols + c;
-                    vcnt[c] -= (nA(o) || (r_counts && nR0(o))) ? 1 : 0;
-                }
-                ++cur_lo;
-            }
-            for (int c = 0; c < cols; ++c) pre[c + 1] = pre[c] + (vcnt[c] > 0 ? 1 : 0);
-            for (int c = 0; c < cols; ++c) {
-                const int b = r * cols + c;
-                if (lossy[b] && jlo[c] <= jhi[c]) sok[b] = pre[jhi[c] + 1] - pre[jlo[c]] > 0 ? 1 : 0;
-            }
-        }
-    }
-    auto usable = [&](int b) -> bool {
+// Smallest band of block rows a plan thread owns: the band's first-row fix-up
+// (below) then never reaches its last row in practice.
+constexpr int kMinBandRows = 16;
+// Grids below this many blocks are planned on one thread (thread start-up
+// costs more than the work).
+constexpr long kParallelMinBlocks = 1L << 16;
+
+// Threads for one plan: requested (0 = FSE_PLAN_THREADS, else the usable CPUs,
+// at most 16), at most one per kMinBandRows block rows.
+// requested > 0 forces that many (tests; bands down to one row), else
+// FSE_PLAN_THREADS or the usable CPUs, at most `cap`.
+int plan_threads(int requested, int cap, int rows, long nb) {
+    if (requested > 0) return std::max(1, std::min(requested, rows));
+    const char *e = getenv("FSE_PLAN_THREADS");
+    int T = e ? atoi(e) : std::min(16, usable_cpus());
+    T = std::min(T, cap);
+    if (nb < kParallelMinBlocks) T = 1;
+    T = std::min(T, rows / kMinBandRows);
+    return std::max(1, T);
+}
+
+// Degeneracy test of conceal.py:53-58 / fse.py:150-151 on the host: does block
+// b's window (its state as of the block's phase) hold a sample of positive
+// weight?  A samples always weigh rho^dist > 0; R samples weigh
+// delta*rho^dist, > 0 iff delta > 0.  `written` marks blocks reconstructed by
+// earlier phases.
+struct Usable {
+    const Geometry &G;
+    const uint8_t *mask;
+    const uint8_t *flag;     // bit 0 LOST, bit 1 RECONSTRUCTED, bit 2 other sample in the block
+    const uint8_t *sok;      // usable whatever was written (window-covered A / R0 block)
+    const uint8_t *written;  // block reconstructed by an earlier phase
+    bool r_counts;           // delta > 0
+    bool operator()(int b) const {
         if (sok[b]) return true;
+        const int B = G.B, cols = G.cols, W = G.W;
         int wr0, wr1, wc0, wc1;
         G.window_rect(b, wr0, wr1, wc0, wc1);
         int br0 = wr0 / B, br1 = (wr1 - 1) / B, bc0 = wc0 / B, bc1 = (wc1 - 1) / B;
@@ -425,8 +357,8 @@ int build_one(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p, in
                     bool inside = or0 >= wr0 && or1 <= wr1 && oc0 >= wc0 && oc1 <= wc1;
                     if (pass == 0) {
                         if (!inside) continue;
-                        if (nA(o)) return true;
-                        if (r_counts && (nR0(o) || (written[o] && nL(o)))) return true;
+                        if (flag[o] & 4) return true;
+                        if (r_counts && ((flag[o] & 2) || (written[o] && (flag[o] & 1)))) return true;
                     } else {
                         if (inside) continue;
                         int y0 = std::max(or0, wr0), y1 = std::min(or1, wr1);
@@ -441,8 +373,714 @@ int build_one(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p, in
                     }
                 }
         return false;
-    };
+    }
+};
 
+// ---- band-parallel optimized order ---------------------------------------------
+//
+// Algorithm 1 (schedule.py:60-105), the snapshot/deferral rule
+// (conceal.py:145-163) and the dependency levels in one pass over the phases,
+// on T threads.  Thread k owns the counts, buckets, ranks and levels of a
+// static band of block rows [s_k, s_k+1).  Per phase:
+//   A  all-reduce of the bands' smallest pending counts: the phase's N_min
+//      (dissemination rounds, no shared counter).  The previous phase's
+//      results become visible (written flags, level rows).
+//   select  select_batch's greedy row-major rule only looks at the row above
+//      and the block to the left, and only candidates (pending blocks of count
+//      N_min) can be taken.  So the selection splits exactly at any row whose
+//      row above holds no candidate: thread k selects rows [b_k, b_k+1), b_k
+//      the first such row at or below s_k (per-row bucket tallies make the test
+//      O(1); a band without one merges into the band above for the phase).
+//   C  barrier; commit_batch: each band applies the count releases that land
+//      in its own rows (from every batch member within one row of them),
+//      decides degeneracy (Usable) and queries its members' levels.
+// Results are identical to the sequential path (tested for many thread counts).
+
+// Dissemination barrier with a min all-reduce folded in (ceil(log2 T)
+// rounds; round i: thread k posts to k + 2^i, waits for k - 2^i).  Epochs
+// only grow, so a slot is never reset.
+struct MinBarrier {
+    struct alignas(64) Slot {
+        std::atomic<uint64_t> v{0};  // epoch << 32 | value
+    };
+    int T, rounds;
+    std::vector<Slot> slots;  // [epoch parity][thread][round]: a thread is never two epochs ahead
+    explicit MinBarrier(int T_) : T(T_), rounds(0) {
+        while ((1 << rounds) < T) ++rounds;
+        slots = std::vector<Slot>((size_t)2 * T * std::max(1, rounds));
+    }
+    // returns the minimum of every thread's `val` of this epoch (epoch >= 1, increasing by 1)
+    int allreduce_min(int k, uint32_t epoch, int val) {
+        Slot *S = &slots[(size_t)(epoch & 1) * T * std::max(1, rounds)];
+        for (int i = 0; i < rounds; ++i) {
+            const int to = (k + (1 << i)) % T;
+            S[(size_t)to * rounds + i].v.store(((uint64_t)epoch << 32) | (uint32_t)val, std::memory_order_release);
+            const std::atomic<uint64_t> &mine = S[(size_t)k * rounds + i].v;
+            uint64_t got;
+            for (int spin = 0; ((got = mine.load(std::memory_order_acquire)) >> 32) < epoch; ++spin) {
+                if (spin < 8192) {
+#if defined(__x86_64__) || defined(__i386__)
+                    __builtin_ia32_pause();
+#endif
+                } else {
+                    std::this_thread::yield();
+                }
+            }
+            val = std::min(val, (int)(uint32_t)got);
+        }
+        return val;
+    }
+};
+
+template <typename CT, typename HT>
+struct BandPlanner {
+    const Geometry &G;
+    const int T, rows, cols, R;
+    const int NC;
+    const std::vector<int> &s;  // band k owns block rows [s[k], s[k+1])
+    CT *cnt;
+    const Usable &usable;
+    uint8_t *written;
+    HT *HL;
+    int32_t *rank;
+    int32_t *level;
+    MinBarrier bar;
+    static constexpr CT kTaken = std::numeric_limits<CT>::max();
+    static constexpr int kNone = INT_MAX;
+
+    struct alignas(64) Band {
+        int r0 = 0, r1 = 0, base = 0, nblk = 0;
+        uint32_t epoch = 0;                // barrier epochs passed
+        std::vector<uint64_t> bits, summ;  // [word][count], summary [sword][count]
+        std::vector<long> bsize;
+        std::vector<int32_t> sel, prev_ok, okb, okptr, deferred, rowbuf;
+        std::vector<uint8_t> lastrow;  // own last row's taken flags after the speculative select
+        int maxlev = -1;
+        bool lastchanged = false;
+        double wait_ms = 0.0, sel_ms = 0.0, fix_ms = 0.0, com_ms = 0.0;  // FSE_PLAN_TIMING
+    };
+    struct alignas(64) Flag {
+        std::atomic<int> v{0};
+    };
+    std::vector<Band> bands;
+    std::vector<Flag> spec_done;  // band k's lastrow of phase ph is published: spec_done[k] = ph + 1
+    std::atomic<int> any_lastchanged{0};
+    std::atomic<int> overflow{0};  // a level does not fit HT: the caller re-plans with int32
+    int n_phases = 0;
+    bool prof = false;
+
+    BandPlanner(const Geometry &G_, int T_, int R_, int NC_, const std::vector<int> &s_, CT *cnt_, const Usable &u,
+                uint8_t *wr, HT *hl, int32_t *rk, int32_t *lv)
+        : G(G_), T(T_), rows(G_.rows), cols(G_.cols), R(R_), NC(NC_), s(s_), cnt(cnt_), usable(u), written(wr),
+          HL(hl), rank(rk), level(lv), bar(T_), bands(T_), spec_done(T_) {}
+
+    int sync_min(int k, int v) { return bar.allreduce_min(k, ++bands[k].epoch, v); }
+
+    // bucket ops on band bd (b: global block index)
+    void add(Band &bd, int c, int b) {
+        const int l = b - bd.base;
+        bd.bits[(size_t)(l >> 6) * NC + c] |= 1ull << (l & 63);
+        bd.summ[(size_t)(l >> 12) * NC + c] |= 1ull << ((l >> 6) & 63);
+        ++bd.bsize[c];
+    }
+    void del(Band &bd, int c, int b) {
+        const int l = b - bd.base;
+        uint64_t &w = bd.bits[(size_t)(l >> 6) * NC + c];
+        w &= ~(1ull << (l & 63));
+        if (!w) bd.summ[(size_t)(l >> 12) * NC + c] &= ~(1ull << ((l >> 6) & 63));
+        --bd.bsize[c];
+    }
+    // blocks of bucket c in the global block range [lo, hi) of band bd, ascending
+    template <class Fn>
+    void scan_range(const Band &bd, int c, int lo, int hi, Fn &&fn) const {
+        int l0 = lo - bd.base, l1 = hi - bd.base;
+        for (int w = l0 >> 6; w <= ((l1 - 1) >> 6); ++w) {
+            uint64_t m = bd.bits[(size_t)w * NC + c];
+            if (w == (l0 >> 6)) m &= ~0ull << (l0 & 63);
+            if (w == ((l1 - 1) >> 6) && ((l1 & 63) != 0)) m &= ~0ull >> (64 - (l1 & 63));
+            while (m) {
+                fn(bd.base + (w << 6) + __builtin_ctzll(m));
+                m &= m - 1;
+            }
+        }
+    }
+
+    void init_band(int k) {
+        Band &bd = bands[k];
+        bd.r0 = s[k];
+        bd.r1 = s[k + 1];
+        bd.base = bd.r0 * cols;
+        bd.nblk = (bd.r1 - bd.r0) * cols;
+        const int words = (bd.nblk + 63) / 64, swords = (words + 63) / 64;
+        bd.bits.assign((size_t)words * NC, 0);
+        bd.summ.assign((size_t)swords * NC, 0);
+        bd.bsize.assign(NC, 0);
+        bd.lastrow.assign(cols, 0);
+        bd.okptr.assign(1, 0);
+        for (int b = bd.base; b < bd.base + bd.nblk; ++b)
+            if (cnt[b] >= 0) add(bd, cnt[b], b);
+    }
+
+    // greedy rule on row r of band bd with the taken flags `up(c)` of row r - 1;
+    // applies the decisions to cnt and returns whether any changed
+    template <class Up>
+    bool redo_row(Band &bd, int nmin, int r, Up &&up) {
+        bool changed = false;
+        int last = -2;  // column of the previous taken block in this row
+        scan_range(bd, nmin, r * cols, (r + 1) * cols, [&](int b) {
+            const int c = b - r * cols;
+            const bool take = last != c - 1 && !(c > 0 && up(c - 1)) && !up(c) && !(c + 1 < cols && up(c + 1));
+            const bool was = cnt[b] == kTaken;
+            if (take) last = c;
+            if (take != was) {
+                cnt[b] = take ? kTaken : (CT)nmin;
+                changed = true;
+            }
+        });
+        return changed;
+    }
+
+    // first-row fix-up of band k against the row above as `up` reports it;
+    // cascades down while rows change, then rebuilds the changed prefix of sel
+    template <class Up>
+    void fixup(int k, int nmin, Up &&up0) {
+        Band &bd = bands[k];
+        int r = bd.r0;
+        if (!redo_row(bd, nmin, r, up0)) return;
+        int last_changed = r;
+        while (r + 1 < bd.r1) {
+            const int ra = r;
+            auto up = [&](int c) { return cnt[(size_t)ra * cols + c] == kTaken; };
+            ++r;
+            if (!redo_row(bd, nmin, r, up)) break;
+            last_changed = r;
+        }
+        if (last_changed == bd.r1 - 1) bd.lastchanged = true;
+        // sel: entries of rows <= last_changed are rebuilt from the taken flags
+        const int lim = (last_changed + 1) * cols;
+        size_t keep = 0;
+        while (keep < bd.sel.size() && bd.sel[keep] < lim) ++keep;
+        bd.rowbuf.clear();
+        scan_range(bd, nmin, bd.r0 * cols, lim, [&](int b) {
+            if (cnt[b] == kTaken) bd.rowbuf.push_back(b);
+        });
+        bd.sel.erase(bd.sel.begin(), bd.sel.begin() + keep);
+        bd.sel.insert(bd.sel.begin(), bd.rowbuf.begin(), bd.rowbuf.end());
+    }
+
+    void release(Band &bd, int o) {
+        if (cnt[o] >= 0) {
+            del(bd, cnt[o], o);
+            if (--cnt[o] >= 0) add(bd, cnt[o], o);
+        }
+    }
+    // releases of batch member b (row rb, column cb) that land in rows [lo, hi)
+    void release_around(Band &bd, int b, int lo, int hi) {
+        const int rb = b / cols, cb = b - rb * cols;
+        for (int rr = std::max(lo, rb - 1); rr <= std::min(hi - 1, rb + 1); ++rr)
+            for (int cc = std::max(0, cb - 1); cc <= std::min(cols - 1, cb + 1); ++cc)
+                if (rr != rb || cc != cb) release(bd, rr * cols + cc);
+    }
+
+    void apply_prev(Band &bd) {
+        for (int b : bd.prev_ok) {
+            written[b] = 1;
+            const int r = b / cols, c = b - r * cols;
+            HT *row = &HL[(size_t)r * cols];
+            const HT lv = (HT)level[b];
+            for (int cc = std::max(0, c - R); cc <= std::min(cols - 1, c + R); ++cc) row[cc] = std::max(row[cc], lv);
+        }
+        bd.prev_ok.clear();
+    }
+
+    void run(int k) {
+        Band &bd = bands[k];
+        init_band(k);
+        using clock = std::chrono::steady_clock;
+        auto tp = prof ? clock::now() : clock::time_point{};
+        auto lapt = [&](double &acc) {
+            if (!prof) return;
+            auto n = clock::now();
+            acc += std::chrono::duration<double, std::milli>(n - tp).count();
+            tp = n;
+        };
+        for (int ph = 0;; ++ph) {
+            // ---- A: the phase's N_min
+            int lm = kNone;
+            for (int c = 0; c < NC; ++c)
+                if (bd.bsize[c]) {
+                    lm = c;
+                    break;
+                }
+            lapt(bd.com_ms);
+            const int nmin = sync_min(k, lm);
+            lapt(bd.wait_ms);
+            apply_prev(bd);
+            if (nmin == kNone) {
+                if (k == 0) n_phases = ph;
+                break;
+            }
+            // ---- speculative select (select_batch, schedule.py:60-82)
+            bd.sel.clear();
+            bd.lastchanged = false;
+            if (bd.bsize[nmin]) {
+                const int swords = (int)(bd.summ.size() / NC);
+                for (int sw = 0; sw < swords; ++sw) {
+                    uint64_t sm = bd.summ[(size_t)sw * NC + nmin];
+                    while (sm) {
+                        const int w = (sw << 6) + __builtin_ctzll(sm);
+                        sm &= sm - 1;
+                        uint64_t m = bd.bits[(size_t)w * NC + nmin];
+                        while (m) {
+                            const int b = bd.base + (w << 6) + __builtin_ctzll(m);
+                            m &= m - 1;
+                            const int r = b / cols, c = b - r * cols;
+                            if (c > 0 && cnt[b - 1] == kTaken) continue;
+                            if (r > bd.r0) {
+                                const int up = b - cols;
+                                if (cnt[up] == kTaken || (c > 0 && cnt[up - 1] == kTaken) ||
+                                    (c + 1 < cols && cnt[up + 1] == kTaken))
+                                    continue;
+                            }
+                            cnt[b] = kTaken;
+                            bd.sel.push_back(b);
+                        }
+                    }
+                }
+            }
+            {
+                const CT *lr = &cnt[(size_t)(bd.r1 - 1) * cols];
+                for (int c = 0; c < cols; ++c) bd.lastrow[c] = lr[c] == kTaken;
+            }
+            spec_done[k].v.store(ph + 1, std::memory_order_release);
+            lapt(bd.sel_ms);
+            // ---- B: fix-up against the band above's speculative last row
+            // (a point-to-point wait: those rows depend on nothing else)
+            if (k > 0 && bd.bsize[nmin]) {
+                const std::atomic<int> &f = spec_done[k - 1].v;
+                for (int spin = 0; f.load(std::memory_order_acquire) < ph + 1; ++spin)
+                    if (spin > 8192) std::this_thread::yield();
+                lapt(bd.wait_ms);
+                const uint8_t *up = bands[k - 1].lastrow.data();
+                fixup(k, nmin, [up](int c) { return up[c] != 0; });
+            }
+            if (bd.lastchanged) any_lastchanged.store(1, std::memory_order_relaxed);
+            lapt(bd.fix_ms);
+            sync_min(k, 0);  // ---- C
+            lapt(bd.wait_ms);
+            if (any_lastchanged.load(std::memory_order_relaxed)) {
+                // a fix-up reached a band's last row, so the band below fixed
+                // up against a stale row: redo every band's fix-up in band
+                // order against the final row above (rare)
+                sync_min(k, 0);
+                if (k == 0) {
+                    for (int q = 1; q < T; ++q) {
+                        const int ra = bands[q].r0 - 1;
+                        fixup(q, nmin, [&](int c) { return cnt[(size_t)ra * cols + c] == kTaken; });
+                    }
+                    any_lastchanged.store(0, std::memory_order_relaxed);
+                }
+                sync_min(k, 0);
+            }
+            // ---- commit_batch (schedule.py:85-94): own members done, then the
+            // releases landing in own rows (own members, the band above's on
+            // its last row, the band below's on its first row)
+            for (int b : bd.sel) {
+                del(bd, nmin, b);
+                cnt[b] = -1;
+            }
+            for (int b : bd.sel) release_around(bd, b, bd.r0, bd.r1);
+            if (k > 0) {
+                const auto &sl = bands[k - 1].sel;
+                for (size_t i = sl.size(); i-- > 0 && sl[i] >= bd.base - cols;) release_around(bd, sl[i], bd.r0, bd.r1);
+            }
+            if (k + 1 < T) {
+                const auto &sl = bands[k + 1].sel;
+                const int lim = bands[k + 1].base + cols;
+                for (size_t i = 0; i < sl.size() && sl[i] < lim; ++i) release_around(bd, sl[i], bd.r0, bd.r1);
+            }
+            // ---- snapshot + degeneracy (conceal.py:145-163) and level queries
+            for (int b : bd.sel) {
+                if (!usable(b)) {
+                    bd.deferred.push_back(b);
+                    continue;
+                }
+                rank[b] = ph;
+                const int r = b / cols, c = b - r * cols;
+                int m = -1;
+                for (int rr = std::max(0, r - R); rr <= std::min(rows - 1, r + R); ++rr)
+                    m = std::max(m, (int)HL[(size_t)rr * cols + c]);
+                level[b] = m + 1;
+                bd.maxlev = std::max(bd.maxlev, m + 1);
+                if (m + 1 >= (int)std::numeric_limits<HT>::max()) overflow.store(1, std::memory_order_relaxed);
+                bd.okb.push_back(b);
+                bd.prev_ok.push_back(b);
+            }
+            bd.okptr.push_back((int32_t)bd.okb.size());
+        }
+    }
+};
+
+// Per-block presence flags (only "any" is ever needed) of block rows [r0, r1):
+// bit 0 a LOST sample (lost_per_block > 0, grid.py:138-144), bit 1 a
+// RECONSTRUCTED sample, bit 2 any other state (class A, grid.py:124-130).
+// Rows are scanned 8 bytes at a time; all-KNOWN and all-LOST words (the common
+// cases) set one bit of their blocks without a per-byte pass.
+void block_flags(const uint8_t *mask, int H, int W, int B, int cols, int r0, int r1, uint8_t *flag) {
+    uint8_t lut[256];
+    for (int v = 0; v < 256; ++v) lut[v] = v == FSE_LOST ? 1 : (v == FSE_RECONSTRUCTED ? 2 : 4);
+    for (int y = r0 * B; y < std::min(H, r1 * B); ++y) {
+        const uint8_t *row = mask + (size_t)y * W;
+        uint8_t *fr = &flag[(size_t)(y / B) * cols];
+        int x = 0;
+        for (; x + 8 <= W; x += 8) {
+            uint64_t w8;
+            std::memcpy(&w8, row + x, 8);
+            if (w8 == 0) {
+                for (int c = x / B; c <= (x + 7) / B; ++c) fr[c] |= 4;
+            } else if (w8 == 0x0101010101010101ull) {  // a run of LOST samples
+                for (int c = x / B; c <= (x + 7) / B; ++c) fr[c] |= 1;
+            } else {
+                for (int i = 0; i < 8; ++i) fr[(x + i) / B] |= lut[row[x + i]];
+            }
+        }
+        for (; x < W; ++x) fr[x / B] |= lut[row[x]];
+    }
+}
+
+// "usable whatever was written" of the lossy blocks of block rows [ra, rb): a
+// block lying wholly inside the window that holds an A sample (or, with
+// delta > 0, a pre-reconstructed sample) makes the window usable.  The fully
+// covered block range of block (r, c)'s window is [ilo(r), ihi(r)] x
+// [jlo(c), jhi(c)], both monotone in their argument, so one row-major sweep
+// with vertical running counts per column and a prefix count along the row
+// answers every block in O(1).
+void sure_usable(const Geometry &G, const uint8_t *flag, const uint8_t *lossy, bool r_counts, int ra, int rb,
+                 uint8_t *sok) {
+    const int B = G.B, rows = G.rows, cols = G.cols, d = G.d;
+    auto lo_hi = [&](int i, int n, int S, int &lo, int &hi) {  // block i of n along an axis of S samples
+        const int s0 = std::max(0, i * B - d);
+        const int s1 = std::min(S, std::min(i * B + B, S) + d);
+        lo = (s0 + B - 1) / B;
+        hi = s1 == S ? n - 1 : s1 / B - 1;
+    };
+    auto good = [&](int o) { return (flag[o] & 4) || (r_counts && (flag[o] & 2)); };
+    std::vector<int> jlo(cols), jhi(cols);
+    for (int c = 0; c < cols; ++c) lo_hi(c, cols, G.W, jlo[c], jhi[c]);
+    std::vector<int32_t> vcnt(cols, 0), pre(cols + 1, 0);
+    int cur_lo = -1, cur_hi = -2;  // block rows summed into vcnt
+    for (int r = ra; r < rb; ++r) {
+        int ilo, ihi;
+        lo_hi(r, rows, G.H, ilo, ihi);
+        if (ilo > ihi) continue;
+        if (cur_lo < 0) cur_lo = ilo, cur_hi = ilo - 1;
+        while (cur_hi < ihi) {
+            ++cur_hi;
+            for (int c = 0; c < cols; ++c) vcnt[c] += good(cur_hi * cols + c) ? 1 : 0;
+        }
+        while (cur_lo < ilo) {
+            for (int c = 0; c < cols; ++c) vcnt[c] -= good(cur_lo * cols + c) ? 1 : 0;
+            ++cur_lo;
+        }
+        for (int c = 0; c < cols; ++c) pre[c + 1] = pre[c] + (vcnt[c] > 0 ? 1 : 0);
+        for (int c = 0; c < cols; ++c) {
+            const int b = r * cols + c;
+            if (lossy[b] && jlo[c] <= jhi[c]) sok[b] = pre[jhi[c] + 1] - pre[jlo[c]] > 0 ? 1 : 0;
+        }
+    }
+}
+
+// init_counts (schedule.py:28-57) of block rows [ra, rb)
+template <typename OutT>
+void init_counts_rows(const uint8_t *lossy, int rows, int cols, int ra, int rb, OutT *counts) {
+    auto h3 = [&](int r, int c) -> int {
+        if (r < 0 || r >= rows) return 0;
+        const uint8_t *p = lossy + (size_t)r * cols;
+        return (c > 0 && p[c - 1] ? 1 : 0) + (p[c] ? 1 : 0) + (c + 1 < cols && p[c + 1] ? 1 : 0);
+    };
+    for (int r = ra; r < rb; ++r) {
+        const int er = (r == 0) + (r == rows - 1);
+        for (int c = 0; c < cols; ++c) {
+            const int self = lossy[(size_t)r * cols + c] ? 1 : 0;
+            if (!self) {
+                counts[(size_t)r * cols + c] = -1;
+                continue;
+            }
+            int n = h3(r - 1, c) + h3(r, c) + h3(r + 1, c) - 1;
+            const int edges = er + (c == 0) + (c == cols - 1);
+            if (edges == 1) n += kMarginBonus;
+            else if (edges >= 2) n += kCornerBonus;
+            counts[(size_t)r * cols + c] = (OutT)n;
+        }
+    }
+}
+
+// Level CSR from the per-block levels (row-major within a level).
+void level_csr(Plan &P, const std::vector<int32_t> &level, int n_levels) {
+    P.level_ptr.assign(n_levels + 1, 0);
+    for (int b : P.batch_blocks) ++P.level_ptr[level[b] + 1];
+    for (int l = 0; l < n_levels; ++l) P.level_ptr[l + 1] += P.level_ptr[l];
+    P.level_blocks.assign(P.n_processed, 0);
+    std::vector<int32_t> fill(P.level_ptr.begin(), P.level_ptr.end() - 1);
+    const int nb = (int)level.size();
+    for (int b = 0; b < nb; ++b)
+        if (level[b] >= 0) P.level_blocks[fill[level[b]]++] = b;
+}
+
+// Retry sweeps (conceal.py:69-94): sequential, row-major, each sees the
+// previous results; every retried block is its own batch.  Levels of retried
+// blocks continue the level rows HL.
+template <typename HT>
+int retry_sweeps(Plan &P, const Usable &usable, uint8_t *written, std::vector<int32_t> deferred, int n_phases,
+                 HT *HL, int32_t *level, int R, int n_levels) {
+    const int rows = P.rows, cols = P.cols;
+    std::sort(deferred.begin(), deferred.end());
+    std::vector<int32_t> pending = deferred, still;
+    int next_rank = n_phases;
+    for (int sweep = 0; sweep < std::max(rows, cols); ++sweep) {
+        if (pending.empty()) break;
+        still.clear();
+        for (int b : pending) {
+            if (usable(b)) {
+                P.rank[b] = next_rank++;
+                written[b] = 1;
+                P.batch_blocks.push_back(b);
+                P.batch_ptr.push_back((int32_t)P.batch_blocks.size());
+                const int r = b / cols, c = b - r * cols;
+                int m = -1;
+                for (int rr = std::max(0, r - R); rr <= std::min(rows - 1, r + R); ++rr)
+                    m = std::max(m, (int)HL[(size_t)rr * cols + c]);
+                level[b] = m + 1;
+                n_levels = std::max(n_levels, m + 2);
+                HT *row = &HL[(size_t)r * cols];
+                for (int cc = std::max(0, c - R); cc <= std::min(cols - 1, c + R); ++cc)
+                    row[cc] = std::max(row[cc], (HT)(m + 1));
+            } else {
+                still.push_back(b);
+            }
+        }
+        if (still.size() == pending.size()) break;
+        pending.swap(still);
+    }
+    P.unconcealed = pending;
+    P.n_processed = (int32_t)P.batch_blocks.size();
+    return n_levels;
+}
+
+template <class T>
+struct RawBuf {  // uninitialised array (filled by the band threads)
+    std::unique_ptr<T[]> p;
+    explicit RawBuf(size_t n) : p(new T[n]) {}
+    T *get() const { return p.get(); }
+};
+
+// Band-parallel plan of the optimized order (see BandPlanner): every stage runs
+// on the T band threads, the few sequential steps (band boundaries, batch
+// offsets, retry sweeps, level offsets) on thread 0 between barriers.
+// Returns false when a level does not fit HT.
+template <typename CT, typename HT>
+bool plan_optimized_parallel(Plan &P, const Geometry &G, int T, const uint8_t *mask, bool r_counts, bool prof) {
+    const int rows = G.rows, cols = G.cols, nb = rows * cols, H = G.H, W = G.W, B = G.B;
+    const int R = (G.d + B - 1) / B;
+    constexpr int NC = 8 + kCornerBonus + 1;  // init_counts' counts are <= 8 + 5
+    auto clk = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    const auto t0 = clk();
+    std::chrono::steady_clock::time_point t1, t2, t3;
+    RawBuf<uint8_t> flag(nb), lossy(nb), sok(nb), written(nb);
+    RawBuf<CT> cnt(nb);
+    RawBuf<HT> HL(nb);
+    RawBuf<int32_t> level(nb);
+    std::vector<int> even(T + 1), s(T + 1), rowlossy(rows);
+    for (int k = 0; k <= T; ++k) even[k] = (int)((long)rows * k / T);
+    P.rank.assign(nb, INT32_MAX);
+    Usable usable{G, mask, flag.get(), sok.get(), written.get(), r_counts};
+    BandPlanner<CT, HT> bp(G, T, R, NC, s, cnt.get(), usable, written.get(), HL.get(), P.rank.data(), level.get());
+    bp.prof = prof;
+    bool ok = true;
+    std::vector<int64_t> bofs, lofs;  // batch / level offsets per (phase or level, band)
+    int n_levels = 0;
+    run_threads(T, [&](int k) {
+        // ---- per-block tallies of even bands (grid.py:138-144)
+        {
+            const int ra = even[k], rb = even[k + 1];
+            std::memset(flag.get() + (size_t)ra * cols, 0, (size_t)(rb - ra) * cols);
+            block_flags(mask, H, W, B, cols, ra, rb, flag.get());
+            for (int r = ra; r < rb; ++r) {
+                int n = 0;
+                for (int b = r * cols; b < (r + 1) * cols; ++b) n += (lossy.get()[b] = flag.get()[b] & 1);
+                rowlossy[r] = n;
+            }
+        }
+        bp.sync_min(k, 0);
+        if (k == 0) {
+            // bands of equal lossy-block count, at least one row each
+            std::vector<long> pre(rows + 1, 0);
+            for (int r = 0; r < rows; ++r) pre[r + 1] = pre[r] + rowlossy[r];
+            P.n_lossy = (int32_t)pre[rows];
+            s[0] = 0;
+            for (int q = 1; q < T; ++q) {
+                const long target = pre[rows] * q / T;
+                int r = (int)(std::lower_bound(pre.begin(), pre.end(), target) - pre.begin());
+                s[q] = std::min(std::max(r, s[q - 1] + 1), rows - (T - q));
+            }
+            s[T] = rows;
+        }
+        bp.sync_min(k, 0);
+        // ---- own rows: counts (schedule.py:28-57), sure-usable flags, level rows
+        {
+            const int ra = s[k], rb = s[k + 1];
+            const size_t o = (size_t)ra * cols, n = (size_t)(rb - ra) * cols;
+            std::memset(sok.get() + o, 0, n);
+            std::memset(written.get() + o, 0, n);
+            std::fill(HL.get() + o, HL.get() + o + n, (HT)-1);
+            std::fill(level.get() + o, level.get() + o + n, -1);
+            init_counts_rows(lossy.get(), rows, cols, ra, rb, cnt.get());
+            sure_usable(G, flag.get(), lossy.get(), r_counts, ra, rb, sok.get());
+        }
+        // ---- the phases (the first all-reduce also orders the inits above)
+        bp.run(k);
+        bp.sync_min(k, 0);
+        if (k == 0) {
+            t1 = clk();
+            ok = !bp.overflow.load();
+            // batches: phase by phase, bands in order (row-major within a phase)
+            const int nph = bp.n_phases;
+            bofs.assign((size_t)nph * T + 1, 0);
+            P.batch_ptr.assign(1, 0);
+            int64_t run = 0;
+            for (int ph = 0; ph < nph; ++ph) {
+                const int64_t before = run;
+                for (int q = 0; q < T; ++q) {
+                    bofs[(size_t)ph * T + q] = run;
+                    run += bp.bands[q].okptr[ph + 1] - bp.bands[q].okptr[ph];
+                }
+                if (run != before) P.batch_ptr.push_back((int32_t)run);
+            }
+            P.batch_blocks.resize(run);
+        }
+        if (!bp.sync_min(k, k == 0 ? (ok ? 1 : 0) : 1)) return;
+        {
+            const auto &bd = bp.bands[k];
+            for (int ph = 0; ph < bp.n_phases; ++ph)
+                std::copy(bd.okb.begin() + bd.okptr[ph], bd.okb.begin() + bd.okptr[ph + 1],
+                          P.batch_blocks.begin() + bofs[(size_t)ph * T + k]);
+        }
+        bp.sync_min(k, 0);
+        if (k == 0) {
+            t2 = clk();
+            std::vector<int32_t> deferred;
+            for (auto &bd : bp.bands) {
+                n_levels = std::max(n_levels, bd.maxlev + 1);
+                deferred.insert(deferred.end(), bd.deferred.begin(), bd.deferred.end());
+            }
+            n_levels = retry_sweeps<HT>(P, usable, written.get(), std::move(deferred), bp.n_phases, HL.get(),
+                                         level.get(), R, n_levels);
+            lofs.assign((size_t)n_levels * T, 0);
+            t3 = clk();
+        }
+        bp.sync_min(k, 0);
+        // ---- level CSR (row-major within a level): counts per (level, band),
+        // offsets, then every band places its own blocks
+        const int32_t *lv = level.get();
+        const int ra = s[k], rb = s[k + 1];
+        std::vector<int64_t> mine(n_levels, 0);
+        for (int b = ra * cols; b < rb * cols; ++b)
+            if (lv[b] >= 0) ++mine[lv[b]];
+        for (int l = 0; l < n_levels; ++l) lofs[(size_t)l * T + k] = mine[l];
+        bp.sync_min(k, 0);
+        if (k == 0) {
+            P.level_ptr.assign(n_levels + 1, 0);
+            int64_t run = 0;
+            for (int l = 0; l < n_levels; ++l) {
+                for (int q = 0; q < T; ++q) {
+                    const int64_t c = lofs[(size_t)l * T + q];
+                    lofs[(size_t)l * T + q] = run;
+                    run += c;
+                }
+                P.level_ptr[l + 1] = (int32_t)run;
+            }
+            P.level_blocks.assign(run, 0);
+        }
+        bp.sync_min(k, 0);
+        for (int l = 0; l < n_levels; ++l) mine[l] = lofs[(size_t)l * T + k];
+        int32_t *out = P.level_blocks.data();
+        for (int b = ra * cols; b < rb * cols; ++b)
+            if (lv[b] >= 0) out[mine[lv[b]]++] = b;
+    });
+    if (!ok) return false;
+    if (prof) {
+        const auto t4 = clk();
+        fprintf(stderr, "plan   %d threads: tallies+phases %.1f ms, merge %.1f ms, retry %.1f ms, level csr %.1f ms\n", T,
+                ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4));
+        for (int k = 0; k < T; ++k)
+            fprintf(stderr, "plan     band %d: wait %.1f select %.1f fixup %.1f commit %.1f ms\n", k, bp.bands[k].wait_ms,
+                    bp.bands[k].sel_ms, bp.bands[k].fix_ms, bp.bands[k].com_ms);
+    }
+    return true;
+}
+
+int build_one(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p, int32_t order, Plan &P,
+              int n_threads, int cap = 1 << 20) {
+    int rc = validate(p, H, W, order);
+    if (rc) return rc;
+    Geometry G{H, W, p->block_size, (H + p->block_size - 1) / p->block_size,
+               (W + p->block_size - 1) / p->block_size, p->d};
+    const int rows = G.rows, cols = G.cols, nb = rows * cols, B = G.B;
+    P.H = H; P.W = W; P.B = B; P.rows = rows; P.cols = cols; P.d = p->d; P.order = order;
+    P.iterations = p->iterations; P.fft1 = p->fft1; P.fft2 = p->fft2;
+    P.rho = p->rho; P.delta = p->delta; P.gamma = p->gamma;
+    const int T = order == FSE_ORDER_OPTIMIZED ? plan_threads(n_threads, cap, rows, nb) : 1;
+    const bool prof = getenv("FSE_PLAN_TIMING") != nullptr;
+    const bool r_counts = p->delta > 0.0;
+    P.max_wr = std::min(H, B + 2 * p->d);
+    P.max_wc = std::min(W, B + 2 * p->d);
+    auto clk = [] { return std::chrono::steady_clock::now(); };
+    auto t_start = clk();
+    auto lap = [&](const char *what) {
+        if (!prof) return;
+        auto now = clk();
+        fprintf(stderr, "plan %-12s %.1f ms\n", what, std::chrono::duration<double, std::milli>(now - t_start).count());
+        t_start = now;
+    };
+    if (T > 1) {
+        // level rows in int16 (half the cache footprint) unless a level
+        // reaches 32767: then again in int32
+        if (!plan_optimized_parallel<int8_t, int16_t>(P, G, T, mask, r_counts, prof))
+            plan_optimized_parallel<int8_t, int32_t>(P, G, T, mask, r_counts, prof);
+        lap("parallel");
+        return FSE_OK;
+    }
+    std::vector<uint8_t> flag(nb, 0), lossy(nb), sok(nb, 0);
+    std::vector<int32_t> counts;
+    if (order == FSE_ORDER_OPTIMIZED) counts.resize(nb);
+    block_flags(mask, H, W, B, cols, 0, rows, flag.data());
+    P.n_lossy = 0;
+    for (int b = 0; b < nb; ++b) {
+        lossy[b] = flag[b] & 1;
+        P.n_lossy += lossy[b];
+    }
+    lap("tallies");
+    if (order == FSE_ORDER_OPTIMIZED) init_counts_rows(lossy.data(), rows, cols, 0, rows, counts.data());
+    sure_usable(G, flag.data(), lossy.data(), r_counts, 0, rows, sok.data());
+    lap("init_counts");
+    std::vector<uint8_t> written(nb, 0);
+    Usable usable{G, mask, flag.data(), sok.data(), written.data(), r_counts};
+
+    // ---- one thread: processing phases in reference order
+    std::vector<int32_t> ph_ptr, ph_blocks;
+    if (order == FSE_ORDER_OPTIMIZED) {
+        rc = schedule_impl(counts.data(), rows, cols, ph_ptr, ph_blocks);
+        if (rc) return rc;
+    } else {
+        ph_ptr.assign(1, 0);
+        for (int b = 0; b < nb; ++b)
+            if (lossy[b]) {
+                ph_blocks.push_back(b);
+                ph_ptr.push_back((int32_t)ph_blocks.size());
+            }
+    }
+    lap("schedule");
     P.rank.assign(nb, INT32_MAX);
     P.batch_ptr.assign(1, 0);
     P.batch_blocks.clear();
@@ -465,28 +1103,30 @@ int build_one(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p, in
         }
     }
     // retry sweeps: sequential, row-major, each sees the previous results
-    std::sort(deferred.begin(), deferred.end());
-    std::vector<int32_t> pending = deferred, still;
-    int next_rank = n_phases;
-    for (int sweep = 0; sweep < std::max(rows, cols); ++sweep) {
-        if (pending.empty()) break;
-        still.clear();
-        for (int b : pending) {
-            if (usable(b)) {
-                P.rank[b] = next_rank++;
-                written[b] = 1;
-                P.batch_blocks.push_back(b);
-                P.batch_ptr.push_back((int32_t)P.batch_blocks.size());
-            } else {
-                still.push_back(b);
+    // (levels of the retried blocks come from the level pass below)
+    {
+        std::sort(deferred.begin(), deferred.end());
+        std::vector<int32_t> pending = deferred, still;
+        int next_rank = n_phases;
+        for (int sweep = 0; sweep < std::max(rows, cols); ++sweep) {
+            if (pending.empty()) break;
+            still.clear();
+            for (int b : pending) {
+                if (usable(b)) {
+                    P.rank[b] = next_rank++;
+                    written[b] = 1;
+                    P.batch_blocks.push_back(b);
+                    P.batch_ptr.push_back((int32_t)P.batch_blocks.size());
+                } else {
+                    still.push_back(b);
+                }
             }
+            if (still.size() == pending.size()) break;
+            pending.swap(still);
         }
-        if (still.size() == pending.size()) break;
-        pending.swap(still);
+        P.unconcealed = pending;
+        P.n_processed = (int32_t)P.batch_blocks.size();
     }
-    P.unconcealed = pending;
-    P.n_processed = (int32_t)P.batch_blocks.size();
-
     lap("ranks");
     // dependency levels over the processing order (level_pass)
     std::vector<int32_t> level(nb, -1);
@@ -494,13 +1134,7 @@ int build_one(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p, in
     const int n_batches = (int)P.batch_ptr.size() - 1;
     int n_levels = n_batches < 32000 ? level_pass<int16_t>(P, rows, cols, R, level)
                                      : level_pass<int32_t>(P, rows, cols, R, level);
-    P.level_ptr.assign(n_levels + 1, 0);
-    for (int b : P.batch_blocks) ++P.level_ptr[level[b] + 1];
-    for (int l = 0; l < n_levels; ++l) P.level_ptr[l + 1] += P.level_ptr[l];
-    P.level_blocks.assign(P.n_processed, 0);
-    std::vector<int32_t> fill(P.level_ptr.begin(), P.level_ptr.end() - 1);
-    for (int b = 0; b < nb; ++b)  // row-major within a level
-        if (level[b] >= 0) P.level_blocks[fill[level[b]]++] = b;
+    level_csr(P, level, n_levels);
     lap("levels");
     return FSE_OK;
 }
@@ -536,13 +1170,14 @@ int fse_schedule_all(const int32_t *counts, int32_t rows, int32_t cols, int32_t 
     return FSE_OK;
 }
 
-int fse_plan_build(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p,
-                   int32_t order, FsePlan **out) {
+static int plan_build(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p, int32_t order,
+                      int32_t n_threads, int32_t cap, FsePlan **out) {
     if (!mask || !out) return fail(FSE_EINVAL, "mask/out is NULL");
+    if (n_threads < 0) return fail(FSE_EINVAL, "n_threads must be >= 0");
     FsePlan *plan = nullptr;
     try {
         plan = new FsePlan();
-        int rc = fse::build_one(mask, H, W, p, order, plan->p);
+        int rc = fse::build_one(mask, H, W, p, order, plan->p, n_threads, cap);
         if (rc) {
             delete plan;
             return rc;
@@ -555,6 +1190,16 @@ int fse_plan_build(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *
     return FSE_OK;
 }
 
+int fse_plan_build(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p,
+                   int32_t order, FsePlan **out) {
+    return plan_build(mask, H, W, p, order, 0, 1 << 20, out);
+}
+
+int fse_plan_build_threads(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p,
+                           int32_t order, int32_t n_threads, FsePlan **out) {
+    return plan_build(mask, H, W, p, order, n_threads, 1 << 20, out);
+}
+
 int fse_plan_build_many(int32_t n, const uint8_t *const *masks, int32_t H, int32_t W,
                         const FseParamsC *p, int32_t order, int32_t n_threads, FsePlan **out) {
     if (n < 0 || (n > 0 && (!masks || !out))) return fail(FSE_EINVAL, "bad arguments");
@@ -563,10 +1208,13 @@ int fse_plan_build_many(int32_t n, const uint8_t *const *masks, int32_t H, int32
     std::vector<int> rcs(n, 0);
     std::vector<std::string> errs(n);
     std::atomic<int> next(0);
+    // frames share the threads: each plan may use the threads the frame
+    // count leaves over (one per plan when frames >= threads)
+    const int per_plan = std::max(1, (n_threads > 0 ? n_threads : (int)std::thread::hardware_concurrency()) / std::max(1, n));
     auto work = [&]() {
         for (int i; (i = next.fetch_add(1)) < n;) {
             out[i] = nullptr;
-            rcs[i] = fse_plan_build(masks[i], H, W, p, order, &out[i]);
+            rcs[i] = plan_build(masks[i], H, W, p, order, 0, per_plan, &out[i]);
             if (rcs[i]) errs[i] = fse_last_error();
         }
     };

@@ -343,3 +343,58 @@ def test_large_golden_batches_from_cpp_planner(golden, name):
     assert plan.unconcealed() == g["unconcealed"].tolist()
     idx = np.searchsorted(g["pick_blocks"], g["sample_blocks"])
     np.testing.assert_array_equal(pick_hash(g["sample_picks"]), g["pick_hash"][idx])
+
+
+def _plan_sig(pl):
+    return pl.batches(), pl.levels(), pl.ranks().tolist(), pl.unconcealed(), pl.n_levels
+
+
+def test_band_parallel_planner_equals_sequential_on_random_masks():
+    """fse_plan_build_threads: the band-parallel planner (per-phase minimum,
+    first-row fix-up, band-local commits, rank + level pass fused) gives the
+    sequential planner's plan for every thread count -- down to bands of one
+    block row, where fix-ups reach the band's last row and the ordered redo
+    path runs."""
+    rng = np.random.default_rng(7)
+    checked = 0
+    for trial in range(60):
+        H, W = int(rng.integers(8, 100)), int(rng.integers(8, 100))
+        B = int(rng.choice([2, 3, 4, 8]))
+        d = int(rng.choice([0, 2, 5, 14]))
+        kind = trial % 4
+        if kind == 0:
+            mask = (rng.random((H, W)) < rng.uniform(0.05, 0.9)).astype(np.uint8)
+        elif kind == 1:
+            bm = rng.random(((H + B - 1) // B, (W + B - 1) // B)) < rng.uniform(0.1, 0.95)
+            mask = np.kron(bm, np.ones((B, B), np.uint8))[:H, :W].astype(np.uint8)
+        elif kind == 2:
+            mask = np.ones((H, W), np.uint8)
+            mask[rng.random((H, W)) < 0.02] = 0
+        else:
+            mask = (rng.random((H, W)) < 0.5).astype(np.uint8)
+            mask[rng.random((H, W)) < 0.1] = 2
+        p = P.FseParams(d=d, iterations=10, block_size=B, delta=float(rng.choice([0.0, 0.2])))
+        ref = _plan_sig(P.build_plan(mask, p, plan_threads=1))
+        rows = (H + B - 1) // B
+        for T in sorted({2, 3, 5, rows}):
+            if T <= rows:
+                assert _plan_sig(P.build_plan(mask, p, plan_threads=T)) == ref, (trial, T)
+                checked += 1
+    assert checked > 150
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg5crop"])
+def test_large_golden_batches_for_every_plan_thread_count(golden, name):
+    from helpers import large_case
+
+    g = golden(f"large_{name}.npz")
+    img, mask, kw, fft = large_case(g)
+    p = P.FseParams(fft_size=fft, **kw)
+    want = csr(g["batch_ptr"], g["batch_blocks"])
+    ref = None
+    for T in (1, 3, 8, 16):
+        pl = P.build_plan(mask, p, plan_threads=T)
+        assert pl.batches() == want, T
+        sig = _plan_sig(pl)
+        ref = ref or sig
+        assert sig == ref, T
