@@ -98,7 +98,7 @@ typedef struct FsePlan FsePlan;
 int fse_plan_build(const uint8_t *mask, int32_t H, int32_t W, const FseParamsC *p,
                    int32_t order, FsePlan **out);
 /* fse_plan_build on n_threads host threads (0 = automatic: FSE_PLAN_THREADS or
- * the usable CPUs for grids of >= 65536 blocks; 1 = the sequential planner).
+ * 3/4 of the usable CPUs for grids of >= 65536 blocks; 1 = the sequential planner).
  * The optimized order is planned by bands of block rows, one per thread, with
  * a per-phase minimum, a first-row fix-up and band-local commits; the plan is
  * identical for every thread count. */

@@ -67,7 +67,7 @@ def lib():
         # local ranks instead of each rank taking all of them
         lws = int(os.environ.get("LOCAL_WORLD_SIZE", "1") or 1)
         if lws > 1 and "FSE_PLAN_THREADS" not in os.environ:
-            os.environ["FSE_PLAN_THREADS"] = str(max(1, len(os.sched_getaffinity(0)) // lws))
+            os.environ["FSE_PLAN_THREADS"] = str(max(1, (3 * len(os.sched_getaffinity(0))) // (4 * lws)))
         L = ctypes.CDLL(LIB_PATH)
         L.fse_last_error.restype = ctypes.c_char_p
         L.fse_version.argtypes = [_pi32, _i32]

@@ -37,8 +37,27 @@
 
 namespace fse {
 
-template <typename T_, int F_, int NW_, bool EXT_ = true, int MINB_ = 0, int CL_ = 1, bool TRACK_ = false>
+// dev instrumentation (-DFSE_CLOCKS): CTA 0, thread 0 records clock64() at the
+// phase boundaries of its window (fse_debug_clocks reads them back)
+#ifdef FSE_CLOCKS
+static __device__ long long g_fse_clk[1024];
+#define FSE_CLK(i)                                                               \
+    do {                                                                         \
+        if (blockIdx.x == 0 && threadIdx.x == 0 && (i) < 1024) g_fse_clk[(i)] = clock64(); \
+    } while (0)
+#else
+#define FSE_CLK(i) \
+    do {           \
+    } while (0)
+#endif
+
+template <typename T_, int F_, int NW_, bool EXT_ = true, int MINB_ = 0, int CL_ = 1, bool TRACK_ = false,
+          int LG_ = 0>
 struct FastCfg {
+    // W gathers of LG bins are issued before their math (0 = the build
+    // default: FSE_LG32 / FSE_LG64); the narrow-level variants, one CTA per SM
+    // with registers to spare, issue all of a thread's gathers at once
+    static constexpr int LGC = LG_;
     // TRACK (fp32): every thread carries its best bin (index, g) through the
     // update and the argmax takes one barrier; otherwise fp32 uses the lazy
     // argmax (running maximum only, candidate warps re-find their bin after a
@@ -393,6 +412,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         N = A.N;
     }
 
+    FSE_CLK(0);
     // ---- e^{+j 2 pi k / F}
     for (int k = t; k < F; k += NT) {
         double s, c;
@@ -480,6 +500,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     for (int off = 16; off; off >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, off);
     if (lane == 0) red[warp] = wsum;
     __syncthreads();
+    FSE_CLK(1);
     double total = 0.0;
 #pragma unroll
     for (int w = 0; w < NW; ++w) total += red[w];
@@ -538,6 +559,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         }
     }
     __syncthreads();
+    FSE_CLK(2);
 
     // ---- bin ownership: warp w owns row segments w + NWT*j: row u0 + RSTEP*j,
     // columns seg*32 + lane (w = the warp's index within the window).
@@ -620,6 +642,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         }
     }
     __syncthreads();
+    FSE_CLK(3);
     partials(Yw);
     __syncthreads();
     // W half rows 0..F/2; with EXT (one CTA per window) also the negative
@@ -765,7 +788,9 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     // products bit-identical); MODE 1 logs p itself
     const T ginv = gamma * inv_tot;
     ArgSlot<T> *asl0 = reinterpret_cast<ArgSlot<T> *>(slots);
+    FSE_CLK(4);
     for (int it = 0; it < I; ++it) {
+        FSE_CLK(8 + 4 * it);
         // ---- (1) CTA-wide argmax (+ runner-up for the guard), one barrier
         FastSlot<T> *sl = slots + (it & 1) * NWT;
         ArgSlot<T> *asl = asl0 + (it & 1) * NWT;
@@ -825,6 +850,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         }
         if constexpr (CL > 1) cooperative_groups::this_cluster().sync();
         else __syncthreads();
+        FSE_CLK(8 + 4 * it + 1);
         int a, b;
         T2 gwin;
         if constexpr (LAZY64) {
@@ -1019,6 +1045,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
                 }
             }
         }
+        FSE_CLK(8 + 4 * it + 2);
         // self-conjugate: gamma * Re(p) * W[k - j] == (gamma Re(p) / 2) (W[k-j] + W[k+j])
         if (selfc) {
             gpr = gpr * (T)0.5;
@@ -1057,7 +1084,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
 #ifndef FSE_LG64
 #define FSE_LG64 1
 #endif
-        constexpr int LG = IS_F32 ? FSE_LG32 : FSE_LG64;
+        constexpr int LG = C::LGC > 0 ? C::LGC : (IS_F32 ? FSE_LG32 : FSE_LG64);
 #pragma unroll
         for (int j0 = 0; j0 < NB; j0 += LG) {
             T2 wl[LG], wh[LG];
@@ -1093,6 +1120,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         }
     }
 
+    FSE_CLK(5);
     // ---- model over the block: sum_it 2 Re(gamma p_it e^{+j 2 pi (a i + b j)/F}),
     // fse.py:159 restricted to the block rect
     if constexpr (MODE == 0) {
@@ -1153,6 +1181,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
             if (pu || pd) __threadfence_system();
         }
     }
+    FSE_CLK(6);
     // keep this CTA's shared memory alive until the cluster is done with it
     if constexpr (CL > 1) cooperative_groups::this_cluster().sync();
 }

@@ -78,12 +78,18 @@ using Fast64T = FastCfg<float, 64, 6, true, 4, 1, true>;
 // 12 warps per window (6 bins per thread) shorten a lone window's iteration --
 // config 2 5.3 -> 5.0 ms; with more windows per level the 6-warp form wins
 // (config 3: 19.8 vs 23.3 ms; 22 warps: slower everywhere)
-using Fast64L = FastCfg<float, 64, 12, true, 2, 1, true>;
+#ifndef FSE_NARROW_LG  // dev knob: gather group of the narrow-level variants
+#define FSE_NARROW_LG 0
+#endif
+#ifndef FSE_NARROW_MINB
+#define FSE_NARROW_MINB 2
+#endif
+using Fast64L = FastCfg<float, 64, 12, true, FSE_NARROW_MINB, 1, true, FSE_NARROW_LG>;
 using Fast32T = FastCfg<float, 32, FSE_F32_32_NW, true, FSE_F32_32_MINB, 1, true>;
 // fp64 levels of at most one window per SM (configs 1 and 2, narrow levels of
 // 3 and 5) with more warps per window (dev knob FSE_F64L = 12 / 22; default 0
 // = the 6-warp kernel: measured config 1 2.1 / 2.2 / 2.1 ms for 12 / 22 / 6)
-using Fast64D12 = FastCfg<double, 64, 12, false, 1>;
+using Fast64D12 = FastCfg<double, 64, 12, false, 1, 1, false, FSE_NARROW_LG>;
 using Fast64D22 = FastCfg<double, 64, 22, false, 1>;
 static int f64_narrow_warps() {
     static const int v = [] {
@@ -292,3 +298,11 @@ int fast_windows(int dtype, int F, const FastArgs &a, int grid, cudaStream_t s) 
 }
 
 }  // namespace fse
+
+#ifdef FSE_CLOCKS
+extern "C" int fse_debug_clocks(long long *out, int n) {
+    return cudaMemcpyFromSymbol(out, fse::g_fse_clk, sizeof(long long) * (size_t)std::min(n, 1024)) == cudaSuccess
+               ? 0
+               : -5;
+}
+#endif
