@@ -591,13 +591,13 @@ def run_small_bench(a, rank, world, local_rank):
         ("optimized", "fp32"), ("linescan", "fp32"), ("optimized", "fp64"), ("linescan", "fp64")]
     res = {f"{o}_{p}": run(o, p) for o, p in combos}
     launches = int(lib.fse_launch_count(1))
-    head = res["optimized_fp64" if a.config == 1 else "optimized_fp32"]
+    head = res["optimized_fp64"]  # the parity path
     if rank == 0:
         line = {
             "metric": "lost_blocks_per_s", "value": head["blocks"] / (head["ms"] * 1e-3), "unit": "blocks/s",
             "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": head["ms"],
             "higher_is_better": True, "scaling": "replicas", "vs_baseline": None,
-            "dtype": "f64" if a.config == 1 else "f32",
+            "dtype": "f64",
             "data": "synthetic (seeded BASELINE generators, paper_2207_00233_b200/synth.py)",
             "config": {"workload": f"config{a.config}: 512x512 synthetic, "
                                    + ("10% isolated" if a.config == 1 else "20% horizontal bursts")

@@ -436,7 +436,7 @@ int fse_run_windows(int32_t n, int32_t M, int32_t N, int32_t F1, int32_t F2, con
     a.picks = picks;
     cudaStream_t s = (cudaStream_t)stream;
     const bool dbg = energies != nullptr;
-    if (!dbg && F1 == F2 && fse::fast_supported(dtype, F1, M, N, 0)) {
+    if (!dbg && F1 == F2 && fse::fast_supported(dtype, F1, M, N, 0, iterations)) {
         fse::FastArgs f{};
         f.values = values;
         f.weights = weights;
@@ -641,7 +641,7 @@ static int session_open(int32_t n, FsePlan *const *plans, void *const *images, c
     a.iterations = p->iterations;
     a.gamma = p->gamma;
     a.picks = picks;
-    S->fast = F1 == F2 && fast_supported(dtype, F1, S->Mmax, S->Nmax, S->model_n);
+    S->fast = F1 == F2 && fast_supported(dtype, F1, S->Mmax, S->Nmax, S->model_n, p->iterations);
     S->guard = S->fast && dtype == FSE_F32 && g_tau0 >= 0.0 && F1 != 128;
     if (S->fast) {
         FastArgs &f = S->f;

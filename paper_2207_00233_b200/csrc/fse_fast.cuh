@@ -51,7 +51,7 @@ static __device__ long long g_fse_clk[1024];
     } while (0)
 #endif
 
-template <typename T_, int F_, int NW_, bool EXT_ = true, int MINB_ = 0, int CL_ = 1, bool TRACK_ = false,
+template <typename T_, int F_, int NW_, int EXT_ = 1, int MINB_ = 0, int CL_ = 1, bool TRACK_ = false,
           int LG_ = 0>
 struct FastCfg {
     // W gathers of LG bins are issued before their math (0 = the build
@@ -75,7 +75,12 @@ struct FastCfg {
     // EXT: row-extended W (rows -F/2..F, no modulo on the gathers).  !EXT: the
     // plain F-row plane with a per-bin wrap select (2/3 of the shared memory;
     // used where the extended plane would cost occupancy, i.e. fp64 at F = 64).
-    static constexpr bool EXT = EXT_;
+    static constexpr bool EXT = EXT_ == 1;
+    // HALF (EXT_ = 2): only the half rows 0..F/2 of W are stored; rows outside
+    // them are read as conj W[-r][-c] (fp64 at F = 128, where even the plain
+    // plane, 129 x 128 x 16 B, exceeds shared memory).  The w-combine writes
+    // W over the row partials, which share its index map.
+    static constexpr bool HALF = EXT_ == 2;
     using T = T_;
     using T2 = typename V2<T_>::type;
     static constexpr int F = F_;
@@ -135,7 +140,7 @@ struct FastLayout {
 
 template <typename T>
 __host__ __device__ inline FastLayout fast_layout(int F, int NW, int Mmax, int Nmax, int model_n,
-                                                  int iters, bool ext = true) {
+                                                  int iters, int ext = 1) {
     FastLayout L;
     const size_t c2 = 2 * sizeof(T);
     size_t o = 0;
@@ -163,7 +168,18 @@ __host__ __device__ inline FastLayout fast_layout(int F, int NW, int Mmax, int N
     L.xs = 2 * yb;
     L.ws = L.xs + xb;
     size_t bigb;
-    if (ext) {
+    if (ext == 2) {
+        // half plane: part (= W after the w-combine, same index map) first,
+        // then Yx, Yw; the staging tiles xs / ws live in part's bytes (dead
+        // once the column pass has read them, before the first partials)
+        L.part = 0;
+        L.yx = pb;
+        L.yw = pb + yb;
+        L.xs = 0;
+        L.ws = xb;
+        bigb = pb + 2 * yb;
+        if (bigb < 2 * xb) bigb = 2 * xb;
+    } else if (ext) {
         // partials live above the W half-plane rows [HS, HE), so the w-plane
         // combine can store W rows directly
         L.part = (2 * yb + 2 * xb > HE) ? 2 * yb + 2 * xb : HE;
@@ -650,13 +666,27 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     // staging bytes below the half rows, while `part` (above them) is still
     // being read by other threads
     constexpr bool MIRROR_NOW = C::EXT && CL == 1;
+    if constexpr (C::HALF) {
+        // in place over the partials (same index map u F + v): a row's four
+        // quarter partials are all read before any of its W entries lands;
+        // the rows of one j are disjoint from every other j's
 #pragma unroll
-    for (int j = 0; j < NB; ++j) {
-        const int u = u0 + RSTEP * j;
-        if (u < R1) {
-            const T2 wv = combine(u);
-            Wext[(u + (C::EXT ? F / 2 : 0)) * F + v] = wv;
-            if (MIRROR_NOW && u >= 1) Wext[(F / 2 - u) * F + ((F - v) & (F - 1))] = T2{wv.x, -wv.y};
+        for (int j = 0; j < NB; ++j) {
+            const int u = u0 + RSTEP * j;
+            T2 wv = T2{0, 0};
+            if (u < R1) wv = combine(u);
+            __syncthreads();
+            if (u < R1) Wext[u * F + v] = wv;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+            const int u = u0 + RSTEP * j;
+            if (u < R1) {
+                const T2 wv = combine(u);
+                Wext[(u + (C::EXT ? F / 2 : 0)) * F + v] = wv;
+                if (MIRROR_NOW && u >= 1) Wext[(F / 2 - u) * F + ((F - v) & (F - 1))] = T2{wv.x, -wv.y};
+            }
         }
     }
     if constexpr (CL > 1) {
@@ -673,7 +703,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         }
     }
     __syncthreads();
-    if constexpr (!C::EXT) {
+    if constexpr (!C::EXT && !C::HALF) {
         // plain plane: rows F/2+1 .. F-1 by W[r][c] = conj W[F-r][-c], and
         // row F = row 0 (the update's row u + a <= F then never wraps)
         for (int idx = t; idx < (F / 2) * F; idx += NT) {
@@ -1068,6 +1098,12 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         const T2 *hi = Wext + (C::EXT ? (y0 + F / 2) * F : y0 * F) + cp;
         const T2 *loW = lo + F * F;  // plain plane: wrapped base
         const int jl = x0 < 0 ? (RSTEP - 1 - x0) / RSTEP : 0;
+        // HALF: row x0 + RSTEP j < 0 reads conj W[-x0 - RSTEP j][(b - v) mod F]
+        // (j < jl), row y0 + RSTEP j > F/2 reads conj W[F - y0 - RSTEP j][(-v - b) mod F]
+        // (j >= jh); offsets, not pointers, since the bases may lie outside the plane
+        const int offLD = x0 * F + cm, offLR = -x0 * F + ((b - v) & (F - 1));
+        const int offHD = y0 * F + cp, offHR = (F - y0) * F + ((-v - b) & (F - 1));
+        const int jh = F / 2 - y0 >= 0 ? (F / 2 - y0) / RSTEP + 1 : 0;
         k1 = 0;
         k2 = 0;
         best = (T)0;
@@ -1093,7 +1129,13 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
                 const int j = j0 + q;
                 const bool inr = j < NB && ((j < NB - 1) || (C::NSEGS % NWT == 0) || (u0 + RSTEP * j < R1));
                 if (inr) {
-                    if constexpr (C::EXT) {
+                    if constexpr (C::HALF) {
+                        const bool rl = j < jl, rh = j >= jh;
+                        wl[q] = Wext[rl ? offLR - j * RSTEP * F : offLD + j * RSTEP * F];
+                        wh[q] = Wext[rh ? offHR - j * RSTEP * F : offHD + j * RSTEP * F];
+                        if (rl) wl[q].y = -wl[q].y;
+                        if (rh) wh[q].y = -wh[q].y;
+                    } else if constexpr (C::EXT) {
                         wl[q] = lo[j * RSTEP * F];
                         wh[q] = hi[j * RSTEP * F];
                     } else {
@@ -1299,7 +1341,7 @@ __global__ void __launch_bounds__(C::NT) fse_fast_dataflow_kernel(const FastArgs
 }
 
 // Host launchers (fse_inst_fast.cu).  dtype FSE_F32/FSE_F64, F = 32/64 (and 128 in fp32).
-int fast_supported(int dtype, int F, int Mmax, int Nmax, int model_n);
+int fast_supported(int dtype, int F, int Mmax, int Nmax, int model_n, int iterations);
 int fast_level(int dtype, int F, bool guard, const FastArgs &a, int grid, int Mmax, int Nmax,
                int model_n, cudaStream_t s);
 int fast_dataflow(int dtype, int F, const FastArgs &a, int Mmax, int Nmax, int model_n,

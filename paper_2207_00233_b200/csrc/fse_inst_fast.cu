@@ -146,7 +146,7 @@ bool cluster_levels() { return cluster_mode() != 0; }
 
 template <class C>
 static int launch_cluster(const FastArgs &a, int windows, int Mmax, int Nmax, int model_n, cudaStream_t s) {
-    const FastLayout L = fast_layout<typename C::T>(C::F, C::NWT, Mmax, Nmax, model_n, a.iterations, C::EXT);
+    const FastLayout L = fast_layout<typename C::T>(C::F, C::NWT, Mmax, Nmax, model_n, a.iterations, C::HALF ? 2 : (C::EXT ? 1 : 0));
     auto kern = fse_fast_cluster_kernel<C>;
     if (int rc = ensure_smem<KTag<C, std::integral_constant<int, 100>>>((const void *)kern, L.total)) return rc;
     if (windows > 0) {
@@ -162,15 +162,24 @@ bool cluster_levels() { return false; }
 // (A 22-warp / 3-bin "latency" variant for levels narrower than the GPU was
 // measured 20% slower on configs 1-2: per-iteration overhead grows with warps.)
 
-int fast_supported(int dtype, int F, int Mmax, int Nmax, int model_n) {
+// F = 128 fp64: half-plane W (65 x 128 x 16 B = 133 KB, the w-combine in
+// place over the partials), 20 warps (13 bins per thread), one CTA per SM.
+using Fast128D = FastCfg<double, 128, 20, 2, 1>;
+
+int fast_supported(int dtype, int F, int Mmax, int Nmax, int model_n, int iterations) {
     // model samples live in registers: at most 2 per thread
-    const bool sizes = F == 32 || F == 64 || (F == 128 && dtype == FSE_F32);
+    bool sizes = F == 32 || F == 64 || F == 128;
+    if (F == 128 && dtype == FSE_F64) {
+        // the half plane leaves room for windows up to ~40 x 40 (B = 8, d <= 16)
+        const FastLayout L = fast_layout<double>(128, Fast128D::NWT, Mmax, Nmax, model_n, iterations, 2);
+        sizes = L.total <= (size_t)227 * 1024;
+    }
     return sizes && Mmax <= F && Nmax <= F && model_n <= 2 * 6 * 32;
 }
 
 template <class C, int MODE, bool GUARD>
 static int launch(const FastArgs &a, int grid, int Mmax, int Nmax, int model_n, cudaStream_t s) {
-    FastLayout L = fast_layout<typename C::T>(C::F, C::NWT, Mmax, Nmax, model_n, a.iterations, C::EXT);
+    FastLayout L = fast_layout<typename C::T>(C::F, C::NWT, Mmax, Nmax, model_n, a.iterations, C::HALF ? 2 : (C::EXT ? 1 : 0));
 #ifdef FSE_SMEM_PAD
     L.total += FSE_SMEM_PAD;  // dev: occupancy sensitivity experiments
 #endif
@@ -186,7 +195,7 @@ static int launch(const FastArgs &a, int grid, int Mmax, int Nmax, int model_n, 
 
 template <class C>
 static int launch_redo(const FastArgs &a, int max_entries, int Mmax, int Nmax, int model_n, cudaStream_t s) {
-    const FastLayout L = fast_layout<typename C::T>(C::F, C::NWT, Mmax, Nmax, model_n, a.iterations, C::EXT);
+    const FastLayout L = fast_layout<typename C::T>(C::F, C::NWT, Mmax, Nmax, model_n, a.iterations, C::HALF ? 2 : (C::EXT ? 1 : 0));
     auto kern = fse_fast_redo_kernel<C, float>;
     if (int rc = ensure_smem<KTag<C, std::integral_constant<int, 101>>>((const void *)kern, L.total)) return rc;
     int per_sm = 0;
@@ -203,7 +212,7 @@ static int launch_redo(const FastArgs &a, int max_entries, int Mmax, int Nmax, i
 
 template <class C, typename IT>
 static int launch_dataflow(const FastArgs &a, int Mmax, int Nmax, int model_n, cudaStream_t s) {
-    const FastLayout L = fast_layout<typename C::T>(C::F, C::NWT, Mmax, Nmax, model_n, a.iterations, C::EXT);
+    const FastLayout L = fast_layout<typename C::T>(C::F, C::NWT, Mmax, Nmax, model_n, a.iterations, C::HALF ? 2 : (C::EXT ? 1 : 0));
     auto kern = fse_fast_dataflow_kernel<C, IT>;
     if (int rc = ensure_smem<KTag<C, IT, std::integral_constant<int, 102>>>((const void *)kern, L.total)) return rc;
     int per_sm = 0;
@@ -233,6 +242,7 @@ int fast_dataflow(int dtype, int F, const FastArgs &a, int Mmax, int Nmax, int m
         if (F == 64) return launch_dataflow<Fast64<float>, float>(a, Mmax, Nmax, model_n, s);
         return launch_dataflow<Fast32<float>, float>(a, Mmax, Nmax, model_n, s);
     }
+    if (F == 128) return launch_dataflow<Fast128D, double>(a, Mmax, Nmax, model_n, s);
     if (F == 64) return launch_dataflow<Fast64<double>, double>(a, Mmax, Nmax, model_n, s);
     return launch_dataflow<Fast32<double>, double>(a, Mmax, Nmax, model_n, s);
 }
@@ -274,6 +284,7 @@ int fast_level(int dtype, int F, bool guard, const FastArgs &a, int grid, int Mm
         return narrow ? launch<Fast32T, 0, false>(a, grid, Mmax, Nmax, model_n, s)
                       : launch<Fast32<float>, 0, false>(a, grid, Mmax, Nmax, model_n, s);
     }
+    if (F == 128) return launch<Fast128D, 0, false>(a, grid, Mmax, Nmax, model_n, s);
     if (F == 64) {
         if (grid <= sms && f64_narrow_warps() == 12) return launch<Fast64D12, 0, false>(a, grid, Mmax, Nmax, model_n, s);
         if (grid <= sms && f64_narrow_warps() == 22) return launch<Fast64D22, 0, false>(a, grid, Mmax, Nmax, model_n, s);
@@ -293,6 +304,7 @@ int fast_windows(int dtype, int F, const FastArgs &a, int grid, cudaStream_t s) 
         if (F == 64) return launch<Fast64<float>, 1, false>(a, grid, a.M, a.N, 0, s);
         return launch<Fast32<float>, 1, false>(a, grid, a.M, a.N, 0, s);
     }
+    if (F == 128) return launch<Fast128D, 1, false>(a, grid, a.M, a.N, 0, s);
     if (F == 64) return launch<Fast64<double>, 1, false>(a, grid, a.M, a.N, 0, s);
     return launch<Fast32<double>, 1, false>(a, grid, a.M, a.N, 0, s);
 }

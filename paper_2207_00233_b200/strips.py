@@ -252,7 +252,8 @@ def open_peer_link(image_dev, rank: int, world: int, dist, group=None):
 def attach_all(executor, link: PeerLink, dist, group=None) -> bool:
     """Attach every rank's shard to its peers, or none: the fused exchange
     needs the fast kernel on every rank (fse_shard_set_peers answers
-    FSE_ENOTSUP otherwise, e.g. fp64 at F = 128 or fft_size=None), so the
+    FSE_ENOTSUP otherwise, e.g. fft_size=None or a window too large for the
+    fp64 F = 128 half plane), so the
     ranks agree through one all_gather and fall back to the collective
     exchange together."""
     rc = link.attach(executor)

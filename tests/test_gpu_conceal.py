@@ -388,7 +388,7 @@ def test_conceal_strips_single_rank_equals_conceal():
 
 
 @pytest.mark.parametrize("config,B,F,iters", [(3, 4, 64, 200), (5, 4, 64, 100), (5, 2, 32, 100),
-                                              (4, 4, 64, 100)])
+                                              (5, 8, 128, 100), (4, 4, 64, 100)])
 def test_full_size_fp64_blocks_match_oracle_on_their_snapshots(config, B, F, iters):
     """Full-size parity without a full-size CPU run: every block's window is a
     pure function of the original mask, the plan ranks and the final values of
@@ -455,7 +455,7 @@ def test_quantize_psnr_epilogue_matches_reference_semantics():
 
 @pytest.mark.parametrize("shape,B,F,prec", [((37, 53), 4, 64, "fp64"), ((10, 12), 4, 32, "fp64"),
                                             ((37, 53), 4, 64, "fp32"), ((70, 45), 8, 128, "fp32"),
-                                            ((33, 31), 2, 32, "fp64")])
+                                            ((70, 45), 8, 128, "fp64"), ((33, 31), 2, 32, "fp64")])
 def test_ragged_and_tiny_frames_fast_path_vs_oracle(shape, B, F, prec):
     """Ragged block grids and frames smaller than a window through the fast
     kernels, against the oracle pipeline (fp64: 1e-6; fp32: PSNR parity)."""
