@@ -87,14 +87,17 @@ using Fast64T = FastCfg<float, 64, 6, true, 4, 1, true>;
 using Fast64L = FastCfg<float, 64, 12, true, FSE_NARROW_MINB, 1, true, FSE_NARROW_LG>;
 using Fast32T = FastCfg<float, 32, FSE_F32_32_NW, true, FSE_F32_32_MINB, 1, true>;
 // fp64 levels of at most one window per SM (configs 1 and 2, narrow levels of
-// 3 and 5) with more warps per window (dev knob FSE_F64L = 12 / 22; default 0
-// = the 6-warp kernel: measured config 1 2.1 / 2.2 / 2.1 ms for 12 / 22 / 6)
+// 3 and 5) with 12 warps per window: a lone window's set-up drops from 40 to
+// 20 us (the 6-warp kernel spills at its 3-CTA register cap), the iteration
+// stays at ~0.7 us (the W gathers bound it); config 1 1.90 -> 1.86 ms, config 2
+// 8.35 -> 8.13 ms (22 warps: 2.02 / 9.05 ms).  FSE_F64L = 0 / 22 selects the
+// 6-warp kernel / the 22-warp variant instead.
 using Fast64D12 = FastCfg<double, 64, 12, false, 1, 1, false, FSE_NARROW_LG>;
 using Fast64D22 = FastCfg<double, 64, 22, false, 1>;
 static int f64_narrow_warps() {
     static const int v = [] {
         const char *e = getenv("FSE_F64L");
-        return e ? atoi(e) : 0;
+        return e ? atoi(e) : 12;
     }();
     return v;
 }
