@@ -605,6 +605,11 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     T2 twr[NR];
 #pragma unroll
     for (int i = 0; i < NR; ++i) twr[i] = tw[(v0 * q4 + tstep * i) & (F - 1)];
+#ifndef FSE_TW_ROT
+#define FSE_TW_ROT 1
+#endif
+    constexpr bool TW_ROT = !IS_F32 && FSE_TW_ROT;
+    const T2 trot = tw[tstep];  // e^{+j 2 pi 4 v0 / F}
     auto partials = [&](const T2 *Y) {
         // (-DFSE_PART_NOUNROLL halves the kernel's code: config 1 fp64 1.9 vs
         // 2.0 ms, but config 4 fp32 +6%, fp64 +0.5%: unrolled by default)
@@ -621,10 +626,21 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
 #pragma unroll
                 for (int i = 0; i < NR; ++i)
                     if (q4 + 4 * i < N) acc = dft_mac(acc, yr[q4 + 4 * i], twr[i]);
-                int k = (v0 * q4 + tstep * NR) & (F - 1);
-                for (int n = q4 + 4 * NR; n < N; n += 4) {
-                    acc = dft_mac(acc, yr[n], tw[k]);
-                    k = (k + tstep) & (F - 1);
+                if constexpr (TW_ROT) {
+                    // fp64: the remaining twiddles by rotation from the last
+                    // register one (per-lane table indices conflict in banks:
+                    // 8% of the kernel's shared wavefronts, 45% excess)
+                    T2 tc = twr[NR - 1];
+                    for (int n = q4 + 4 * NR; n < N; n += 4) {
+                        tc = T2{fma(tc.x, trot.x, -tc.y * trot.y), fma(tc.x, trot.y, tc.y * trot.x)};
+                        acc = dft_mac(acc, yr[n], tc);
+                    }
+                } else {
+                    int k = (v0 * q4 + tstep * NR) & (F - 1);
+                    for (int n = q4 + 4 * NR; n < N; n += 4) {
+                        acc = dft_mac(acc, yr[n], tw[k]);
+                        k = (k + tstep) & (F - 1);
+                    }
                 }
                 part[(u * 4 + q4) * QW + v0] = acc;
             }
