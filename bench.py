@@ -615,7 +615,7 @@ def run_small_bench(a, rank, world, local_rank):
 
 def run_strips_bench(a, rank, world, local_rank):
     """BASELINE config 5: one 3840x2160 frame, 50% burst losses, B in {2,4,8}
-    (FFT 32/64/128), 100 iterations, fp32, spatially strip-sharded over the
+    (FFT 32/64/128), 100 iterations, --precision (fp64 default), spatially strip-sharded over the
     ranks (paper_2207_00233_b200.strips).  A step = host plan (every rank, same
     global plan) + shard levels with halo exchanges + result gather to rank 0."""
     import torch
@@ -631,7 +631,7 @@ def run_strips_bench(a, rank, world, local_rank):
                          fft_size=Fk)
     img, mask = synth.config_scene(5)
     H, W = mask.shape
-    src = torch.from_numpy(img).cuda().float()
+    src = torch.from_numpy(img).cuda().to(torch.float32 if a.precision == "fp32" else torch.float64)
     msk = torch.from_numpy(mask).cuda()
     work = torch.empty_like(src)
     out = torch.empty_like(msk)
@@ -704,7 +704,7 @@ def run_strips_bench(a, rank, world, local_rank):
         # GPU (same kernels; untimed)
         whole = src.clone()
         wout = torch.empty_like(msk)
-        P.run_frames_device([P.build_plan(mask, params)], [whole], [msk], [wout], params, "fp32")
+        P.run_frames_device([P.build_plan(mask, params)], [whole], [msk], [wout], params, a.precision)
         torch.cuda.synchronize()
         strips_equal = bool(torch.equal(whole, work))
     if rank == 0:
@@ -713,10 +713,10 @@ def run_strips_bench(a, rank, world, local_rank):
         line = {
             "metric": "lost_blocks_per_s", "value": blocks * a.steps / (ms * 1e-3), "unit": "blocks/s",
             "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms / a.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32" if a.precision == "fp32" else "f64",
             "data": "synthetic (seeded BASELINE generators, paper_2207_00233_b200/synth.py)",
             "config": {"workload": f"config5: 3840x2160 synthetic luma, 50% burst 16x16 losses, FSE "
-                                   f"{Bk}x{Bk} / d=14 / FFT {Fk}x{Fk} / 100 it, optimized order, fp32, "
+                                   f"{Bk}x{Bk} / d=14 / FFT {Fk}x{Fk} / 100 it, optimized order, {a.precision}, "
                                    f"strip-sharded", "block": Bk, "fft": Fk,
                        "parallelism": f"row bands x{world}, halo exchange: "
                                       + ("fused peer stores + device flags" if link is not None

@@ -157,6 +157,30 @@ class DeviceContext:
         return t
 
 
+def check_device_frames(images_dev, masks_dev, plans, precision: str, block_size: int) -> None:
+    """The C ABI takes raw pointers: the working images must be contiguous 2-D
+    CUDA tensors of the precision's type (float32 / float64) whose block grid is
+    the plan's, the masks uint8 of the same shape -- anything else would be
+    read as the wrong type or past the end."""
+    import torch
+
+    if precision not in PRECISIONS:
+        raise ValueError(f"precision must be one of {PRECISIONS}")
+    if len(images_dev) != len(plans) or len(masks_dev) != len(plans):
+        raise ValueError("one image and one mask per plan")
+    want = torch.float32 if precision == "fp32" else torch.float64
+    for i, (t, m, P) in enumerate(zip(images_dev, masks_dev, plans)):
+        if t.dtype != want:
+            raise ValueError(f"image {i} is {t.dtype}, precision {precision!r} needs {want}")
+        if not (t.is_cuda and t.is_contiguous() and m.is_cuda and m.is_contiguous()):
+            raise ValueError(f"image/mask {i} must be contiguous CUDA tensors")
+        if t.dim() != 2 or m.dtype != torch.uint8 or tuple(m.shape) != tuple(t.shape):
+            raise ValueError(f"image/mask {i} must be 2-D of one shape, the mask uint8")
+        H, W = t.shape
+        if (-(-H // block_size), -(-W // block_size)) != (P.rows, P.cols):
+            raise ValueError(f"image {i} of {H}x{W} does not match the plan's {P.rows}x{P.cols} blocks")
+
+
 def run_frames_device(plans, images_dev, masks_dev, masks_out_dev, params: FseParams,
                       precision: str, picks_dev=None, stream=None) -> None:
     """Run the level pipeline on device tensors already in HBM (the `value` path)."""
@@ -165,6 +189,7 @@ def run_frames_device(plans, images_dev, masks_dev, masks_out_dev, params: FsePa
     n = len(plans)
     if n == 0:
         return
+    check_device_frames(images_dev, masks_dev, plans, precision, params.block_size)
     P0 = plans[0]
     F = params.fft_dims((P0.max_wr, P0.max_wc))
     if params.fft_size is not None and (F[0] < P0.max_wr or F[1] < P0.max_wc):

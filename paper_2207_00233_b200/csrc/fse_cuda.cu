@@ -470,6 +470,11 @@ struct FseShard {
     size_t n_entries = 0;
     std::vector<int> lvl_off;  // entry offset of (group g, level l) at g * n_levels + l
     std::vector<int32_t> edge;  // per level: bit0 top zone, bit1 bottom zone touched
+    // fused halo exchange: before level l the upper (lower) neighbour must have
+    // finished its levels < need_up[l] (need_down[l]) -- the highest level,
+    // plus one, among the neighbour's blocks that this band's level-l windows
+    // read as reconstructed (lower rank, within the dependency radius); 0 = none
+    std::vector<int32_t> need_up, need_down;
     unsigned char *dev = nullptr;
     size_t off_ent = 0, off_cnt = 0, off_next = 0, off_done = 0, off_queue = 0, off_redo = 0;
     bool fast = false, guard = false, masks_out = false;
@@ -568,6 +573,34 @@ static int session_open(int32_t n, FsePlan *const *plans, void *const *images, c
         }
     S->lvl_off[(size_t)groups * n_levels] = (int)n_entries;
     S->n_entries = n_entries;
+    // cross-band dependency levels of a shard (one frame): per level, the
+    // neighbour levels its windows actually wait for
+    S->need_up.assign(n_levels, 0);
+    S->need_down.assign(n_levels, 0);
+    if (n == 1 && (row_lo > 0 || row_hi < P0.rows)) {
+        const Plan &P = P0;
+        std::vector<int32_t> lev(nb, -1);
+        for (int l = 0; l + 1 < (int)P.level_ptr.size(); ++l)
+            for (int i = P.level_ptr[l]; i < P.level_ptr[l + 1]; ++i) lev[P.level_blocks[i]] = l;
+        auto zone = [&](int r0z, int r1z, int nr0, int nr1, std::vector<int32_t> &need) {
+            // own blocks of rows [r0z, r1z) against neighbour rows [nr0, nr1)
+            for (int r = std::max(r0z, row_lo); r < std::min(r1z, row_hi); ++r)
+                for (int c = 0; c < cols; ++c) {
+                    const int b = r * cols + c;
+                    if (lev[b] < 0) continue;
+                    const int rb = P.rank[b];
+                    int m = need[lev[b]];
+                    for (int rr = std::max(nr0, r - R); rr <= std::min(nr1 - 1, r + R); ++rr)
+                        for (int cc = std::max(0, c - R); cc <= std::min(cols - 1, c + R); ++cc) {
+                            const int o = rr * cols + cc;
+                            if (lev[o] >= 0 && P.rank[o] < rb) m = std::max(m, lev[o] + 1);
+                        }
+                    need[lev[b]] = m;
+                }
+        };
+        if (row_lo > 0) zone(row_lo, row_lo + R, std::max(0, row_lo - R), row_lo, S->need_up);
+        if (row_hi < P0.rows) zone(row_hi - R, row_hi, row_hi, std::min(P0.rows, row_hi + R), S->need_down);
+    }
     // one device staging buffer:
     //   uploaded: frame table | ranks | entries (level order)
     //   zeroed:   redo counters | work/queue counters | dependency counters
@@ -785,10 +818,19 @@ static int session_run(FseShard *S, int l0, int l1, bool whole, cudaStream_t s) 
             if (rc == FSE_OK && S->sig_up) rc = peer_wait(S->own_flags + 0, S->base, s);
             if (rc == FSE_OK && S->sig_down) rc = peer_wait(S->own_flags + 1, S->base, s);
         }
+        // level l waits only for the neighbour levels its windows read
+        // (need_*; values only grow, so a target at or below one already
+        // waited for is skipped): interior levels run without any wait
+        uint32_t waited_up = 0, waited_down = 0;
         for (int l = l0; l < l1 && rc == FSE_OK; ++l) {
-            if (l > 0) {
-                if (S->sig_up) rc = peer_wait(S->own_flags + 0, S->base + (uint32_t)l, s);
-                if (rc == FSE_OK && S->sig_down) rc = peer_wait(S->own_flags + 1, S->base + (uint32_t)l, s);
+            const uint32_t nu = (uint32_t)S->need_up[l], nd = (uint32_t)S->need_down[l];
+            if (S->sig_up && nu > waited_up) {
+                rc = peer_wait(S->own_flags + 0, S->base + nu, s);
+                waited_up = nu;
+            }
+            if (rc == FSE_OK && S->sig_down && nd > waited_down) {
+                rc = peer_wait(S->own_flags + 1, S->base + nd, s);
+                waited_down = nd;
             }
             const int2 *lvl = reinterpret_cast<const int2 *>(dev + S->off_ent) + S->lvl_off[l];
             const int cnt = S->lvl_off[l + 1] - S->lvl_off[l];

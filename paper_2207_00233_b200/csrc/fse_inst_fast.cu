@@ -172,6 +172,9 @@ using Fast128D = FastCfg<double, 128, 20, 2, 1>;
 int fast_supported(int dtype, int F, int Mmax, int Nmax, int model_n, int iterations) {
     // model samples live in registers: at most 2 per thread
     bool sizes = F == 32 || F == 64 || F == 128;
+#ifdef FSE_NO_F128_F64  // dev A/B: fp64 F = 128 on the generic kernel, as before the half plane
+    if (F == 128 && dtype == FSE_F64) return 0;
+#endif
     if (F == 128 && dtype == FSE_F64) {
         // the half plane leaves room for windows up to ~40 x 40 (B = 8, d <= 16)
         const FastLayout L = fast_layout<double>(128, Fast128D::NWT, Mmax, Nmax, model_n, iterations, 2);

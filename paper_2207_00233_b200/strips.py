@@ -129,6 +129,9 @@ class ShardExecutor:
                  precision: str, stream=None):
         import torch
 
+        from .conceal import check_device_frames
+
+        check_device_frames([image_dev], [mask_dev], [plan], precision, params.block_size)
         self.stream = stream if stream is not None else torch.cuda.current_stream().cuda_stream
         dim = max(plan.max_wr, plan.max_wc, 1)
         self._decay = DeviceContext.decay(params, dim)

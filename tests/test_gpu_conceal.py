@@ -634,3 +634,30 @@ def test_conceal_batch_64_frames_fp64_matches_reference_frame0(golden):
         o1, m1, _ = P.conceal(imgs[f], msks[f], p, "optimized", precision="fp64")
         np.testing.assert_array_equal(out[f], o1)
         np.testing.assert_array_equal(om[f], m1)
+
+
+@pytest.mark.gpu
+def test_device_entry_points_reject_mismatched_buffers():
+    """run_frames_device / ShardExecutor hand raw pointers to the C ABI: a
+    working image of the wrong type (fp32 buffer for the fp64 path), shape or
+    layout is rejected before any launch, never read as the wrong type."""
+    import torch
+    from paper_2207_00233_b200 import strips
+
+    img, mask = synth.config_scene(1)
+    p = P.FseParams(d=14, iterations=5, block_size=4, fft_size=64)
+    plan = P.build_plan(mask, p)
+    m = torch.from_numpy(mask).cuda()
+    out = torch.empty_like(m)
+    f32 = torch.from_numpy(img).cuda().float()
+    with pytest.raises(ValueError, match="precision"):
+        P.run_frames_device([plan], [f32], [m], [out], p, "fp64")
+    with pytest.raises(ValueError, match="precision"):
+        strips.ShardExecutor(plan, (0, plan.rows), f32, m, out, p, "fp64")
+    f64 = f32.double()
+    with pytest.raises(ValueError, match="does not match"):
+        P.run_frames_device([plan], [f64[:-8]], [m[:-8]], [out], p, "fp64")
+    with pytest.raises(ValueError, match="contiguous"):
+        P.run_frames_device([plan], [f64.t()], [m.t()], [out], p, "fp64")
+    P.run_frames_device([plan], [f64], [m], [out], p, "fp64")  # the matching call runs
+    torch.cuda.synchronize()
