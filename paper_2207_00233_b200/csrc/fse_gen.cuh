@@ -28,25 +28,27 @@
 
 namespace fse {
 
-template <typename T_, int NW_, int NB_>
+template <typename T_, int NW_, int NB_, int MINB_ = 0>
 struct GenCfg {
     using T = T_;
     using T2 = typename V2<T_>::type;
     static constexpr int NW = NW_;
     static constexpr int NT = NW_ * 32;
-    static constexpr int NB = NB_;  // canonical bins per thread
+    static constexpr int NB = NB_;      // canonical bins per thread
+    static constexpr int MINB = MINB_;  // __launch_bounds__ min blocks per SM
 };
 
 constexpr int GEN_WPT = 8;  // W half-plane outputs per thread (one round)
 
 struct GenLayout {
-    size_t tw1, tw2, slots, model, big, yx, yw, xs, ws, total;
+    size_t tw1, tw2, slots, model, hist, big, yx, yw, xs, ws, total;
 };
 
 // Shared memory: twiddles, argmax slots, the block model, then one region
 // used in turn for the staging tiles + column spectra and for the W plane.
 template <typename T>
-__host__ __device__ inline GenLayout gen_layout(int F1, int F2, int Mmax, int Nmax, int NW, int model_n) {
+__host__ __device__ inline GenLayout gen_layout(int F1, int F2, int Mmax, int Nmax, int NW, int model_n,
+                                                int iters) {
     GenLayout L;
     const size_t c2 = 2 * sizeof(T);
     auto a16 = [](size_t x) { return (x + 15) & ~size_t(15); };
@@ -55,6 +57,7 @@ __host__ __device__ inline GenLayout gen_layout(int F1, int F2, int Mmax, int Nm
     L.tw2 = o; o = a16(o + (size_t)F2 * c2);
     L.slots = o; o = a16(o + 2 * (size_t)NW * sizeof(ArgSlot<double>));
     L.model = o; o = a16(o + (size_t)(model_n > 0 ? model_n : 1) * sizeof(T));
+    L.hist = o; o = a16(o + (size_t)(iters > 0 ? iters : 1) * sizeof(PickRec<T>));
     o = (o + 127) & ~size_t(127);
     L.big = o;
     const size_t H = (size_t)F1 / 2;
@@ -123,6 +126,7 @@ __device__ __forceinline__ void gen_window(const KArgs &A, const GenLayout &L, u
     T2 *tw2 = reinterpret_cast<T2 *>(sm + L.tw2);
     ArgSlot<T> *slots = reinterpret_cast<ArgSlot<T> *>(sm + L.slots);
     T *model = reinterpret_cast<T *>(sm + L.model);
+    PickRec<T> *hist = reinterpret_cast<PickRec<T> *>(sm + L.hist);
     unsigned char *big = sm + L.big;
     T2 *Yx = reinterpret_cast<T2 *>(big + L.yx);
     T2 *Yw = reinterpret_cast<T2 *>(big + L.yw);
@@ -220,6 +224,9 @@ __device__ __forceinline__ void gen_window(const KArgs &A, const GenLayout &L, u
         bu[j] = u;
         bv[j] = v;
     }
+    int uF2[NB];  // row offset of each bin in the W plane
+#pragma unroll
+    for (int j = 0; j < NB; ++j) uF2[j] = bu[j] * F2;
     auto row_dft = [&](const T2 *Y, int u, int v) -> T2 {  // sum_n Y[u][n] e^{-j 2 pi v n / F2}
         const T2 *yr = Y + u * N;
         T2 acc = T2{0, 0};
@@ -295,7 +302,7 @@ __device__ __forceinline__ void gen_window(const KArgs &A, const GenLayout &L, u
             const T e = energy(G[j]);
             if (bu[j] >= 0 && e > best) {
                 best = e;
-                blin = (unsigned)(bu[j] * F2 + bv[j]);
+                blin = ((unsigned)bu[j] << 16) | (unsigned)bv[j];
                 bg = G[j];
             }
         }
@@ -322,16 +329,12 @@ __device__ __forceinline__ void gen_window(const KArgs &A, const GenLayout &L, u
         // no bin above 0 (all energies 0 or NaN): the reference's strict-'>'
         // scan from -1 keeps (0, 0) (_kernel.pyx:32-44), whose g is 0
         if (glin == 0xFFFFFFFFu) glin = 0;
-        const int a = (int)(glin / (unsigned)F2), b = (int)glin - a * F2;
+        // bins are tagged (u << 16) | v: row-major order without a division
+        const int a = (int)(glin >> 16), b = (int)(glin & 0xFFFFu);
         const T2 gwin = T2{asl[gw].gre, asl[gw].gim};
-        T gpr, gpi;
-        if constexpr (IS_F32) {
-            gpr = gwin.x * ginv;
-            gpi = gwin.y * ginv;
-        } else {
-            gpr = gamma * div_by(gwin.x, tot, inv_tot);
-            gpi = gamma * div_by(gwin.y, tot, inv_tot);
-        }
+        // p = g / sum(w) (_kernel.pyx:46-47) with gamma / sum(w) folded into
+        // one factor, as in the power-of-two kernel (fse_fast.cuh)
+        T gpr = gwin.x * ginv, gpi = gwin.y * ginv;
         if (t == 0 && picks_out) {
             picks_out[2 * it] = a;
             picks_out[2 * it + 1] = b;
@@ -346,19 +349,15 @@ __device__ __forceinline__ void gen_window(const KArgs &A, const GenLayout &L, u
             }
         }
         // self-conjugate: gamma Re(p) W[k - j] == (gamma Re(p) / 2)(W[k-j] + W[k+j])
-        const bool selfc = small_mod(2 * a, F1, inv1) == 0 && small_mod(2 * b, F2, inv2) == 0;
+        // (canonical picks have 0 <= a <= F1/2 and 0 <= b < F2)
+        const bool selfc = (a == 0 || 2 * a == F1) && (b == 0 || 2 * b == F2);
         if (selfc) {
             gpr = gpr * (T)0.5;
             gpi = (T)0;
         }
-        // block model: 2 Re(gamma p e^{+j 2 pi (a i / F1 + b j / F2)}) (fse.py:159)
+        // the pick for the block model, synthesised after the loop
         if constexpr (MODE == 0) {
-            for (int q = t; q < nsamp; q += NT) {
-                const int mi = br0 + q / bw, mj = bc0 + q % bw;
-                const T2 p1 = tw1[small_mod(a * mi, F1, inv1)], p2 = tw2[small_mod(b * mj, F2, inv2)];
-                const T c = p1.x * p2.x - p1.y * p2.y, s = p1.x * p2.y + p1.y * p2.x;
-                model[q] += (T)2 * (gpr * c - gpi * s);
-            }
+            if (t == 0) hist[it] = PickRec<T>{a, b, gpr, gpi};
         }
         if (it + 1 == I) break;  // the last spectrum update is never observed
 
@@ -370,37 +369,47 @@ __device__ __forceinline__ void gen_window(const KArgs &A, const GenLayout &L, u
 #pragma unroll
         for (int j = 0; j < NB; ++j) {
             if (bu[j] >= 0) {
-                const int u = bu[j], v = bv[j];
+                const int v = bv[j];
                 int cm = v - b;
                 cm += cm < 0 ? F2 : 0;
                 int cp = v + b;
                 cp -= cp >= F2 ? F2 : 0;
-                const T2 lo = rowlo[u * F2 + cm], hi = rowhi[u * F2 + cp];
+                const T2 lo = rowlo[uF2[j] + cm], hi = rowhi[uF2[j] + cp];
                 if constexpr (IS_F32) G[j] = spectral_update_bc(G[j], lo, hi, -gpr, gpi);
                 else G[j] = spectral_update(G[j], lo, hi, T2{-gpr, -gpr}, T2{gpi, -gpi});
                 const T e = energy(G[j]);
                 if (e > best) {
                     best = e;
-                    blin = (unsigned)(u * F2 + v);
+                    blin = ((unsigned)bu[j] << 16) | (unsigned)v;
                     bg = G[j];
                 }
             }
         }
     }
 
-    // ---- write-back of the block's LOST samples (conceal.py:61-66)
+    // ---- block model 2 Re(gamma p e^{+j 2 pi (a i / F1 + b j / F2)}) summed in
+    // iteration order (fse.py:159 restricted to the block), then the write-back
+    // of the block's LOST samples (conceal.py:61-66)
     if constexpr (MODE == 0) {
         __syncthreads();
         IT *img = reinterpret_cast<IT *>(fd->image);
         for (int q = t; q < nsamp; q += NT) {
+            const int mi = br0 + q / bw, mj = bc0 + q % bw;
+            T acc = (T)0;
+            for (int it = 0; it < I; ++it) {
+                const PickRec<T> h = hist[it];
+                const T2 p1 = tw1[small_mod(h.a * mi, F1, inv1)], p2 = tw2[small_mod(h.b * mj, F2, inv2)];
+                const T c = p1.x * p2.x - p1.y * p2.y, sn = p1.x * p2.y + p1.y * p2.x;
+                acc += (T)2 * (h.gpr * c - h.gpi * sn);
+            }
             const size_t off = (size_t)(wr0 + br0 + q / bw) * A.W + (wc0 + bc0 + q % bw);
-            if (fd->mask[off] == FSE_LOST) img[off] = (IT)model[q];
+            if (fd->mask[off] == FSE_LOST) img[off] = (IT)acc;
         }
     }
 }
 
 template <class C, int MODE>
-__global__ void __launch_bounds__(C::NT) fse_gen_kernel(const KArgs A, const GenLayout L) {
+__global__ void __launch_bounds__(C::NT, C::MINB) fse_gen_kernel(const KArgs A, const GenLayout L) {
     extern __shared__ __align__(128) unsigned char sm[];
     gen_window<C, MODE, typename C::T>(A, L, sm);
 }

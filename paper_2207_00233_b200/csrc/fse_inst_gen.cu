@@ -10,6 +10,13 @@ namespace fse {
 // bins) sit one per SM on their dependency levels, so a window's latency, not
 // the SM's throughput, sets the time; NB covers up to 384 * NB bins.
 template <typename T, int NB> using Gen = GenCfg<T, 12, NB>;
+// windows of up to 1,280 canonical bins (the reference default 48 x 48 has
+// 1,154): 8 warps x 5 bins at two CTAs per SM, so a dependency level of up
+// to 2 x SMs windows is one wave
+#ifndef FSE_GEN_NARROW8
+#define FSE_GEN_NARROW8 1
+#endif
+template <typename T> using Gen8 = GenCfg<T, 8, 5, 2>;
 
 static int gen_dev() {
     int d = 0;
@@ -24,7 +31,7 @@ template <class C, int MODE>
 static int launch_gen(const KArgs &a, int grid, int Mmax, int Nmax, int F1max, int F2max, int model_n,
                       cudaStream_t s) {
     using T = typename C::T;
-    const GenLayout L = gen_layout<T>(F1max, F2max, Mmax, Nmax, C::NW, model_n);
+    const GenLayout L = gen_layout<T>(F1max, F2max, Mmax, Nmax, C::NW, model_n, a.iterations);
     auto kern = fse_gen_kernel<C, MODE>;
     static std::atomic<size_t> configured[64] = {};
     const int dev = gen_dev();
@@ -53,6 +60,8 @@ static int pick(const KArgs &a, int grid, int Mmax, int Nmax, int F1, int F2, in
     const long bins = (long)(F2 / 2 + 1) * (F1 % 2 == 0 ? 2 : 1) + (long)((F1 - 1) / 2) * F2;
     const long wout = (long)(F1 / 2 + 1) * F2;
     if (wout > (long)NT * GEN_WPT) return fail(FSE_ENOTSUP, "any-size kernel: W half plane too large");
+    if (FSE_GEN_NARROW8 && bins <= 5L * Gen8<T>::NT && wout <= (long)Gen8<T>::NT * GEN_WPT)
+        return launch_gen<Gen8<T>, MODE>(a, grid, Mmax, Nmax, F1, F2, model_n, s);
     if (bins <= 4L * NT) return launch_gen<Gen<T, 4>, MODE>(a, grid, Mmax, Nmax, F1, F2, model_n, s);
     if (bins <= 8L * NT) return launch_gen<Gen<T, 8>, MODE>(a, grid, Mmax, Nmax, F1, F2, model_n, s);
     return fail(FSE_ENOTSUP, "any-size kernel: too many bins");
