@@ -61,7 +61,11 @@ static int ensure_smem(const void *kern, size_t bytes) {
 // min blocks/SM in __launch_bounds__ pins the register budget to the occupancy
 // the shared memory allows (an explicit 1 lets ptxas take 121 registers and
 // halves the fp32 occupancy)
-template <typename T> using Fast64 = FastCfg<T, 64, 6, sizeof(T) == 4, sizeof(T) == 4 ? 4 : 3>;  // fp64: plain W plane
+#ifndef FSE_F64_NW  // dev knob: warps per window of the wide fp64 F = 64 kernel
+#define FSE_F64_NW 6
+#endif
+template <typename T>
+using Fast64 = FastCfg<T, 64, sizeof(T) == 4 ? 6 : FSE_F64_NW, sizeof(T) == 4, sizeof(T) == 4 ? 4 : 3>;  // fp64: plain W plane
 
 // F = 32 fp32: 3 warps per window (6 bins per thread), 8 CTAs per SM --
 // config 5 B=2 (1.04M windows of 30x30): 95 ms vs 120 ms with 6 warps
