@@ -74,8 +74,13 @@ using Fast64 = FastCfg<T, 64, sizeof(T) == 4 ? 6 : FSE_F64_NW, sizeof(T) == 4, s
 #define FSE_F32_32_NW 3
 #define FSE_F32_32_MINB 8
 #endif
+#ifndef FSE_F64_32_NW  // dev knobs: the fp64 F = 32 kernel
+#define FSE_F64_32_NW 6
+#define FSE_F64_32_MINB 0
+#endif
 template <typename T>
-using Fast32 = FastCfg<T, 32, sizeof(T) == 4 ? FSE_F32_32_NW : 6, true, sizeof(T) == 4 ? FSE_F32_32_MINB : 0>;
+using Fast32 = FastCfg<T, 32, sizeof(T) == 4 ? FSE_F32_32_NW : FSE_F64_32_NW, true,
+                       sizeof(T) == 4 ? FSE_F32_32_MINB : FSE_F64_32_MINB>;
 // tracked-argmax fp32 twins for narrow levels (see FastCfg::TRACK)
 using Fast64T = FastCfg<float, 64, 6, true, 4, 1, true>;
 // levels of at most one window per SM (config 2; config 5 bands at N = 8):
@@ -96,7 +101,9 @@ using Fast32T = FastCfg<float, 32, FSE_F32_32_NW, true, FSE_F32_32_MINB, 1, true
 // stays at ~0.7 us (the W gathers bound it); config 1 1.90 -> 1.86 ms, config 2
 // 8.35 -> 8.13 ms (22 warps: 2.02 / 9.05 ms).  FSE_F64L = 0 / 22 selects the
 // 6-warp kernel / the 22-warp variant instead.
-using Fast64D12 = FastCfg<double, 64, 12, false, 1, 1, false, FSE_NARROW_LG>;
+// (gathers in groups of 3 bins: a lone window's update loop 971 -> 926 cycles
+// per iteration, profiles/r2/narrow_lg_ab_r2h.jsonl)
+using Fast64D12 = FastCfg<double, 64, 12, false, 1, 1, false, FSE_NARROW_LG ? FSE_NARROW_LG : 3>;
 using Fast64D22 = FastCfg<double, 64, 22, false, 1>;
 static int f64_narrow_warps() {
     static const int v = [] {
@@ -171,7 +178,10 @@ bool cluster_levels() { return false; }
 
 // F = 128 fp64: half-plane W (65 x 128 x 16 B = 133 KB, the w-combine in
 // place over the partials), 20 warps (13 bins per thread), one CTA per SM.
-using Fast128D = FastCfg<double, 128, 20, 2, 1>;
+#ifndef FSE_F128D_LG
+#define FSE_F128D_LG 0
+#endif
+using Fast128D = FastCfg<double, 128, 20, 2, 1, 1, false, FSE_F128D_LG>;
 
 int fast_supported(int dtype, int F, int Mmax, int Nmax, int model_n, int iterations) {
     // model samples live in registers: at most 2 per thread
