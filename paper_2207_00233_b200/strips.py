@@ -96,10 +96,12 @@ def run_levels(executor, image, rank: int, world: int, bands, flags_all, n_level
     row slices are contiguous views, sent and received in place.  Returns the
     number of halo messages this rank sent."""
     sent = 0
+    if world == 1:  # nothing to exchange: every level in one C++ call
+        if n_levels:
+            executor.run(0, n_levels)
+        return 0
     for l in range(n_levels):
         executor.run(l)
-        if world == 1:
-            continue
         sends, recvs = exchange_plan(rank, world, bands, flags_all, l, R, B, H)
         if not sends and not recvs:
             continue
@@ -150,8 +152,10 @@ class ShardExecutor:
         _lib.check(_lib.lib().fse_shard_levels(self.handle, ctypes.byref(n), _lib.ptr32(fl)))
         self.flags = fl[: self.n_levels]
 
-    def run(self, level: int) -> None:
-        _lib.check(_lib.lib().fse_shard_run(self.handle, level, level + 1, self.stream))
+    def run(self, level: int, level_hi: int | None = None) -> None:
+        """Launch levels [level, level_hi) (default: the one level) in one call."""
+        hi = level + 1 if level_hi is None else level_hi
+        _lib.check(_lib.lib().fse_shard_run(self.handle, level, hi, self.stream))
 
     def close(self) -> None:
         if self.handle is not None and self.handle.value:

@@ -81,11 +81,12 @@ class EmuExecutor:
         self.n_levels = len(self.levels)
         self.flags = strips.edge_flags(self.levels, self.cols, band, strips.halo_rows(params))
 
-    def run(self, level):
+    def run(self, level, level_hi=None):
         lo, hi = self.band
-        for b in self.levels[level]:
-            if lo <= b // self.cols < hi:
-                emulate_block(self.image, self.mask, b, self.ranks, self.owner, B, self.p)
+        for lv in range(level, level + 1 if level_hi is None else level_hi):
+            for b in self.levels[lv]:
+                if lo <= b // self.cols < hi:
+                    emulate_block(self.image, self.mask, b, self.ranks, self.owner, B, self.p)
 
 
 def _worker(rank, world, port, out):
