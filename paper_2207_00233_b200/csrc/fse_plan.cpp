@@ -404,10 +404,15 @@ struct Usable {
 // Dissemination barrier with a min all-reduce folded in (ceil(log2 T)
 // rounds; round i: thread k posts to k + 2^i, waits for k - 2^i).  Epochs
 // only grow, so a slot is never reset.
+// A band thread that fails (std::bad_alloc) sets `abort`; threads waiting in a
+// barrier see it and unwind too, so no thread waits forever.
+struct PlanAborted {};
+
 struct MinBarrier {
     struct alignas(64) Slot {
         std::atomic<uint64_t> v{0};  // epoch << 32 | value
     };
+    std::atomic<bool> abort{false};
     int T, rounds;
     std::vector<Slot> slots;  // [epoch parity][thread][round]: a thread is never two epochs ahead
     explicit MinBarrier(int T_) : T(T_), rounds(0) {
@@ -428,6 +433,7 @@ struct MinBarrier {
                     __builtin_ia32_pause();
 #endif
                 } else {
+                    if (abort.load(std::memory_order_relaxed)) throw PlanAborted{};
                     std::this_thread::yield();
                 }
             }
@@ -664,7 +670,10 @@ struct BandPlanner {
             if (k > 0 && bd.bsize[nmin]) {
                 const std::atomic<int> &f = spec_done[k - 1].v;
                 for (int spin = 0; f.load(std::memory_order_acquire) < ph + 1; ++spin)
-                    if (spin > 8192) std::this_thread::yield();
+                    if (spin > 8192) {
+                        if (bar.abort.load(std::memory_order_relaxed)) throw PlanAborted{};
+                        std::this_thread::yield();
+                    }
                 lapt(bd.wait_ms);
                 const uint8_t *up = bands[k - 1].lastrow.data();
                 fixup(k, nmin, [up](int c) { return up[c] != 0; });
@@ -905,7 +914,9 @@ bool plan_optimized_parallel(Plan &P, const Geometry &G, int T, const uint8_t *m
     bool ok = true;
     std::vector<int64_t> bofs, lofs;  // batch / level offsets per (phase or level, band)
     int n_levels = 0;
+    std::atomic<bool> failed{false};
     run_threads(T, [&](int k) {
+      try {
         // ---- per-block tallies of even bands (grid.py:138-144)
         {
             const int ra = even[k], rb = even[k + 1];
@@ -1012,7 +1023,13 @@ bool plan_optimized_parallel(Plan &P, const Geometry &G, int T, const uint8_t *m
         int32_t *out = P.level_blocks.data();
         for (int b = ra * cols; b < rb * cols; ++b)
             if (lv[b] >= 0) out[mine[lv[b]]++] = b;
+      } catch (const PlanAborted &) {
+      } catch (...) {  // std::bad_alloc: unwind every band thread
+        failed.store(true);
+        bp.bar.abort.store(true);
+      }
     });
+    if (failed.load()) throw std::bad_alloc();
     if (!ok) return false;
     if (prof) {
         const auto t4 = clk();
