@@ -1225,14 +1225,22 @@ int fse_plan_build_threads(const uint8_t *mask, int32_t H, int32_t W, const FseP
 int fse_plan_build_many(int32_t n, const uint8_t *const *masks, int32_t H, int32_t W,
                         const FseParamsC *p, int32_t order, int32_t n_threads, FsePlan **out) {
     if (n < 0 || (n > 0 && (!masks || !out))) return fail(FSE_EINVAL, "bad arguments");
-    int nt = n_threads > 0 ? n_threads : (int)std::thread::hardware_concurrency();
-    nt = std::max(1, std::min(nt, n));
+    // host threads: the caller's count, else FSE_PLAN_THREADS (set per local
+    // rank under torchrun), else the usable CPUs (frames are independent: the
+    // frame workers never wait on each other)
+    int all = n_threads;
+    if (all <= 0) {
+        const char *e = getenv("FSE_PLAN_THREADS");
+        all = e ? std::max(1, atoi(e)) : fse::usable_cpus();
+    }
+    int nt = std::max(1, std::min(all, n));
     std::vector<int> rcs(n, 0);
     std::vector<std::string> errs(n);
     std::atomic<int> next(0);
-    // frames share the threads: each plan may use the threads the frame
-    // count leaves over (one per plan when frames >= threads)
-    const int per_plan = std::max(1, (n_threads > 0 ? n_threads : (int)std::thread::hardware_concurrency()) / std::max(1, n));
+    // frames share the threads: each plan may use the band threads the frame
+    // count leaves over (3/4 of them: band threads spin), one when frames >=
+    // threads
+    const int per_plan = std::max(1, (all - all / 4) / std::max(1, n));
     auto work = [&]() {
         for (int i; (i = next.fetch_add(1)) < n;) {
             out[i] = nullptr;
