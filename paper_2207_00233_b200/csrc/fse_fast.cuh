@@ -1247,6 +1247,12 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
 template <class C, int MODE, bool GUARD>
 __global__ void __launch_bounds__(C::NT, C::MINB) fse_fast_kernel(const FastArgs A, const FastLayout L) {
     extern __shared__ __align__(128) unsigned char sm[];
+    // programmatic dependent launch (level launches, fse_inst_fast.cu): let the
+    // next level's grid be scheduled now, and wait for the previous level's
+    // grid (complete, memory visible) before touching global memory -- the
+    // launch gap between dependent levels overlaps this level's work
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     fast_window<C, MODE, GUARD, typename C::T>(A, L, blockIdx.x, sm);
 }
 

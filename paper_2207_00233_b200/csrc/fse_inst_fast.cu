@@ -200,6 +200,19 @@ int fast_supported(int dtype, int F, int Mmax, int Nmax, int model_n, int iterat
     return sizes && Mmax <= F && Nmax <= F && model_n <= 2 * 6 * 32;
 }
 
+// Level launches with programmatic dependent launch (FSE_PDL=1; the kernel
+// waits for the previous grid in the stream before any global access).  Off by
+// default: measured slower -- config 1 1.86 vs 1.80 ms, config 2 fp32 5.96 vs
+// 5.30 ms, config 5 B=2 fp64 163.9 vs 160.8 ms (the next level's early CTAs
+// hold SM slots while they wait); only config 2 fp64 gained (7.69 vs 7.81 ms).
+static bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("FSE_PDL");
+        return e && atoi(e) != 0;
+    }();
+    return on;
+}
+
 template <class C, int MODE, bool GUARD>
 static int launch(const FastArgs &a, int grid, int Mmax, int Nmax, int model_n, cudaStream_t s) {
     FastLayout L = fast_layout<typename C::T>(C::F, C::NWT, Mmax, Nmax, model_n, a.iterations, C::HALF ? 2 : (C::EXT ? 1 : 0));
@@ -209,7 +222,21 @@ static int launch(const FastArgs &a, int grid, int Mmax, int Nmax, int model_n, 
     auto kern = fse_fast_kernel<C, MODE, GUARD>;
     if (int rc = ensure_smem<KTag<C, std::integral_constant<int, MODE>, std::integral_constant<bool, GUARD>>>((const void *)kern, L.total)) return rc;
     if (grid > 0) {
-        kern<<<grid, C::NT, L.total, s>>>(a, L);
+        if (pdl_enabled()) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(grid);
+            cfg.blockDim = dim3(C::NT);
+            cfg.dynamicSmemBytes = L.total;
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            FSE_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, a, L));
+        } else {
+            kern<<<grid, C::NT, L.total, s>>>(a, L);
+        }
         FSE_CUDA_TRY(cudaGetLastError());
         g_launches.fetch_add(1, std::memory_order_relaxed);
     }
