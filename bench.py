@@ -76,6 +76,8 @@ def args_():
     ap.add_argument("--frames", type=int, default=64)
     ap.add_argument("--guard", default=None,
                     help="fp32 near-tie guard 'tau0,tau1' or 'off' (default: library default)")
+    ap.add_argument("--plan-on", default="rank0", choices=["rank0", "all"],
+                    help="config 5 at N>1: plan the frame on rank 0 and broadcast it (default), or on every rank")
     ap.add_argument("--halo", default="p2p", choices=["p2p", "collective"],
                     help="config 5 at N>1: fused halo stores over peer memory (default) or per-level "
                          "send/recv over torch.distributed")
@@ -643,11 +645,15 @@ def run_strips_bench(a, rank, world, local_rank):
     # (None on every rank when some rank cannot map its neighbours: the
     # per-level collective exchange then runs instead, and the line says so)
     link = strips.open_peer_link(work, rank, world, dist, grp) if world > 1 and a.halo == "p2p" else None
+    hg = strips.host_group(dist, grp) if world > 1 and a.plan_on == "rank0" else None
 
     def step():
         work.copy_(src)
         t0 = time.perf_counter()
-        plan = P.build_plan(mask, params)
+        if hg is not None:  # plan once, broadcast the bytes over a host (gloo) group
+            plan = strips.broadcast_plan(mask, params, "optimized", rank, dist, hg, 0)
+        else:
+            plan = P.build_plan(mask, params)
         processed = (plan.ranks() != np.iinfo(np.int32).max).reshape(plan.rows, plan.cols)
         bands = strips.band_partition(processed.sum(axis=1), world, R)
         stats["plan_ms"] = 1e3 * (time.perf_counter() - t0)
@@ -720,7 +726,8 @@ def run_strips_bench(a, rank, world, local_rank):
                                    f"strip-sharded", "block": Bk, "fft": Fk,
                        "parallelism": f"row bands x{world}, halo exchange: "
                                       + ("fused peer stores + device flags" if link is not None
-                                         else "per-level send/recv" if world > 1 else "none")},
+                                         else "per-level send/recv" if world > 1 else "none")
+                                      + (", plan on rank 0 + broadcast" if hg is not None else "")},
             "lost_mpixel_per_s": float((mask == 1).sum()) * a.steps / (ms * 1e-3) / 1e6,
             "blocks_per_step": blocks, "levels_per_step": stats["levels"],
             "host_plan_ms_per_step": stats["plan_ms"], "halo_messages_rank0": stats["halo_msgs"],

@@ -121,6 +121,12 @@ int fse_plan_levels(const FsePlan *plan, int32_t *ptr, int32_t *blocks);
 int fse_plan_ranks(const FsePlan *plan, int32_t *rank);
 /* ConcealReport.unconcealed_blocks, row-major */
 int fse_plan_unconcealed(const FsePlan *plan, int32_t *blocks);
+/* A plan as bytes (ranks, batch and level CSRs, unconcealed list, geometry and
+ * parameters): one rank plans a large frame and broadcasts them, the other
+ * ranks import instead of re-planning (strips.py).  export_size < 0 = error. */
+int64_t fse_plan_export_size(const FsePlan *plan);
+int fse_plan_export(const FsePlan *plan, void *buf, int64_t size);
+int fse_plan_import(const void *buf, int64_t size, FsePlan **out);
 
 /* fsefill.schedule.init_counts (schedule.py:28-57): lossy[rows*cols] != 0 marks
  * a lossy block; counts[rows*cols] out. */

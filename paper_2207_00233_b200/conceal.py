@@ -84,6 +84,24 @@ class Plan:
         _lib.check(_lib.lib().fse_plan_ranks(self.handle, _lib.ptr32(r)))
         return r
 
+    def to_bytes(self) -> bytes:
+        """The plan serialised (fse_plan_export): broadcast it instead of planning
+        the same frame on every rank."""
+        n = int(_lib.lib().fse_plan_export_size(self.handle))
+        if n < 0:
+            _lib.check(n)
+        buf = (ctypes.c_ubyte * n)()
+        _lib.check(_lib.lib().fse_plan_export(self.handle, buf, n))
+        return bytes(buf)
+
+    @classmethod
+    def from_bytes(cls, data) -> "Plan":
+        """A plan from fse_plan_export's bytes (fse_plan_import)."""
+        a = np.frombuffer(bytes(data), dtype=np.uint8)
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().fse_plan_import(a.ctypes.data, a.size, ctypes.byref(h)))
+        return cls(h.value)
+
     def unconcealed(self) -> list:
         u = np.zeros(max(self.n_unconcealed, 1), dtype=np.int32)
         _lib.check(_lib.lib().fse_plan_unconcealed(self.handle, _lib.ptr32(u)))

@@ -1309,4 +1309,86 @@ int fse_plan_unconcealed(const FsePlan *plan, int32_t *blocks) {
     return FSE_OK;
 }
 
+// Serialised plan: int32 header, three doubles, then the rank table and the
+// batch / level CSRs and the unconcealed list.  One rank plans a frame and
+// broadcasts these bytes; the others import them (strips.py).
+static const int32_t kPlanMagic = 0x46534550;  // "FSEP"
+static const int kPlanHdr = 24;
+
+int64_t fse_plan_export_size(const FsePlan *plan) {
+    if (!plan) return fail(FSE_EINVAL, "NULL plan");
+    const fse::Plan &P = plan->p;
+    const size_t n = P.rank.size() + P.batch_ptr.size() + P.batch_blocks.size() + P.level_ptr.size() +
+                     P.level_blocks.size() + P.unconcealed.size();
+    return (int64_t)(kPlanHdr * sizeof(int32_t) + 3 * sizeof(double) + n * sizeof(int32_t));
+}
+
+int fse_plan_export(const FsePlan *plan, void *buf, int64_t size) {
+    if (!plan || !buf) return fail(FSE_EINVAL, "NULL argument");
+    if (size < fse_plan_export_size(plan)) return fail(FSE_EINVAL, "export buffer too small");
+    const fse::Plan &P = plan->p;
+    int32_t h[kPlanHdr] = {kPlanMagic, 1, P.H, P.W, P.B, P.rows, P.cols, P.d, P.order, P.iterations,
+                           P.fft1, P.fft2, P.n_lossy, P.n_processed, P.max_wr, P.max_wc,
+                           (int32_t)P.rank.size(), (int32_t)P.batch_ptr.size(), (int32_t)P.batch_blocks.size(),
+                           (int32_t)P.level_ptr.size(), (int32_t)P.level_blocks.size(),
+                           (int32_t)P.unconcealed.size(), 0, 0};
+    unsigned char *o = static_cast<unsigned char *>(buf);
+    auto put = [&](const void *src, size_t bytes) {
+        if (bytes) std::memcpy(o, src, bytes);
+        o += bytes;
+    };
+    put(h, sizeof(h));
+    const double dd[3] = {P.rho, P.delta, P.gamma};
+    put(dd, sizeof(dd));
+    for (const std::vector<int32_t> *v : {&P.rank, &P.batch_ptr, &P.batch_blocks, &P.level_ptr, &P.level_blocks,
+                                          &P.unconcealed})
+        put(v->data(), v->size() * sizeof(int32_t));
+    return FSE_OK;
+}
+
+int fse_plan_import(const void *buf, int64_t size, FsePlan **out) {
+    if (!buf || !out) return fail(FSE_EINVAL, "NULL argument");
+    if (size < (int64_t)(kPlanHdr * sizeof(int32_t) + 3 * sizeof(double))) return fail(FSE_EINVAL, "truncated plan");
+    const unsigned char *in = static_cast<const unsigned char *>(buf);
+    int32_t h[kPlanHdr];
+    std::memcpy(h, in, sizeof(h));
+    if (h[0] != kPlanMagic || h[1] != 1) return fail(FSE_EINVAL, "not a serialised plan");
+    for (int i = 16; i < 22; ++i)
+        if (h[i] < 0) return fail(FSE_EINVAL, "corrupt plan header");
+    const int64_t need = (int64_t)(kPlanHdr * sizeof(int32_t) + 3 * sizeof(double)) +
+                         (int64_t)sizeof(int32_t) * ((int64_t)h[16] + h[17] + h[18] + h[19] + h[20] + h[21]);
+    if (size < need) return fail(FSE_EINVAL, "truncated plan");
+    if ((int64_t)h[5] * h[6] != h[16] || h[17] < 1 || h[19] < 1) return fail(FSE_EINVAL, "inconsistent plan");
+    FsePlan *plan = nullptr;
+    try {
+        plan = new FsePlan();
+        fse::Plan &P = plan->p;
+        P.H = h[2]; P.W = h[3]; P.B = h[4]; P.rows = h[5]; P.cols = h[6]; P.d = h[7]; P.order = h[8];
+        P.iterations = h[9]; P.fft1 = h[10]; P.fft2 = h[11]; P.n_lossy = h[12]; P.n_processed = h[13];
+        P.max_wr = h[14]; P.max_wc = h[15];
+        in += sizeof(h);
+        double dd[3];
+        std::memcpy(dd, in, sizeof(dd));
+        in += sizeof(dd);
+        P.rho = dd[0]; P.delta = dd[1]; P.gamma = dd[2];
+        int k = 16;
+        for (std::vector<int32_t> *v : {&P.rank, &P.batch_ptr, &P.batch_blocks, &P.level_ptr, &P.level_blocks,
+                                        &P.unconcealed}) {
+            v->resize(h[k++]);
+            if (!v->empty()) std::memcpy(v->data(), in, v->size() * sizeof(int32_t));
+            in += v->size() * sizeof(int32_t);
+        }
+        if (P.batch_ptr.back() != (int32_t)P.batch_blocks.size() ||
+            P.level_ptr.back() != (int32_t)P.level_blocks.size()) {
+            delete plan;
+            return fail(FSE_EINVAL, "inconsistent plan CSR");
+        }
+    } catch (const std::exception &e) {
+        delete plan;
+        return fail(FSE_ENOMEM, e.what());
+    }
+    *out = plan;
+    return FSE_OK;
+}
+
 }  // extern "C"

@@ -27,8 +27,52 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from .conceal import DeviceContext, build_plan
+from .conceal import DeviceContext, Plan, build_plan
 from .fse import FseParams
+
+
+_HOST_GROUPS: dict = {}
+
+
+def host_group(dist, group=None):
+    """A gloo group over the same ranks (host-side collectives: plan bytes,
+    flags), created once; `group` itself when it is already gloo."""
+    if dist.get_backend(group) == "gloo":
+        return group
+    key = None if group is None else tuple(dist.get_process_group_ranks(group))
+    g = _HOST_GROUPS.get(key)
+    if g is None:
+        g = dist.new_group(ranks=None if key is None else list(key), backend="gloo")
+        _HOST_GROUPS[key] = g
+    return g
+
+
+def broadcast_plan(mask, params: FseParams, order: str, rank: int, dist, group=None, src: int = 0,
+                   plan_threads: int = 0):
+    """Plan the frame on rank `src` only and broadcast the plan's bytes
+    (fse_plan_export / fse_plan_import) -- instead of every rank planning the
+    same frame with its share of the host CPUs.  `group` must carry CPU
+    tensors (gloo), so waiting ranks block in the transport, not on a GPU
+    stream.  `plan_threads` is the planning rank's thread count (0 = 3/4 of
+    the usable CPUs: the other ranks are idle meanwhile)."""
+    import os
+
+    import torch
+
+    if rank == src:
+        T = plan_threads or max(1, (3 * len(os.sched_getaffinity(0))) // 4)
+        plan = build_plan(mask, params, order, plan_threads=T)
+        data = plan.to_bytes()
+        n = torch.tensor([len(data)], dtype=torch.int64)
+    else:
+        n = torch.zeros(1, dtype=torch.int64)
+    dist.broadcast(n, src, group=group)
+    if rank == src:
+        t = torch.from_numpy(np.frombuffer(data, dtype=np.uint8).copy())
+    else:
+        t = torch.empty(int(n.item()), dtype=torch.uint8)
+    dist.broadcast(t, src, group=group)
+    return plan if rank == src else Plan.from_bytes(t.numpy().tobytes())
 
 
 def halo_rows(params: FseParams) -> int:
@@ -305,14 +349,18 @@ def run_levels_collective(executor, image_dev, rank, world, bands, R, B, H, dist
 
 
 def conceal_strips(image, mask, params: FseParams, precision: str = "fp64", order: str = "optimized",
-                   group=None, gather: bool = True, transport: str = "p2p"):
+                   group=None, gather: bool = True, transport: str = "p2p", plan_on: str = "rank0"):
     """Conceal one frame on all ranks of the default process group (one GPU per
     rank).  Returns (image, mask) numpy arrays on rank 0 when gather=True (other
-    ranks get None), else this rank's band rows and its band.  transport "p2p"
+    ranks get None), else this rank's band rows and its band.  plan_on "rank0"
+    = rank 0 plans the frame and broadcasts the plan (broadcast_plan), "all" =
+    every rank plans it (deterministic, identical).  transport "p2p"
     = fused halo exchange over peer memory (PeerLink), "collective" = per-level
     send/recv over torch.distributed (NCCL on GPUs)."""
     if transport not in ("p2p", "collective"):
         raise ValueError("transport must be 'p2p' or 'collective'")
+    if plan_on not in ("rank0", "all"):
+        raise ValueError("plan_on must be 'rank0' (plan once, broadcast) or 'all' (every rank plans)")
     import torch
     import torch.distributed as dist
 
@@ -320,7 +368,12 @@ def conceal_strips(image, mask, params: FseParams, precision: str = "fp64", orde
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     mask = np.ascontiguousarray(mask, dtype=np.uint8)
     H, W = mask.shape
-    plan = build_plan(mask, params, order)
+    if world > 1 and plan_on == "rank0":
+        hg = host_group(dist, group)
+        src = 0 if group is None else dist.get_global_rank(group, 0)
+        plan = broadcast_plan(mask, params, order, rank, dist, hg, src)
+    else:
+        plan = build_plan(mask, params, order)
     B = params.block_size
     R = halo_rows(params)
     processed = (plan.ranks() != np.iinfo(np.int32).max).reshape(plan.rows, plan.cols)

@@ -398,3 +398,21 @@ def test_large_golden_batches_for_every_plan_thread_count(golden, name):
         sig = _plan_sig(pl)
         ref = ref or sig
         assert sig == ref, T
+
+
+def test_plan_export_import_round_trip_and_rejects_corrupt_bytes():
+    """fse_plan_export / fse_plan_import (one rank plans, the others import):
+    the imported plan is the plan; truncated or foreign bytes are rejected."""
+    from paper_2207_00233_b200 import synth
+
+    _, mask = synth.config_scene(3)
+    p = P.FseParams(d=14, iterations=10, block_size=4, fft_size=64)
+    a = P.build_plan(mask, p)
+    data = a.to_bytes()
+    b = P.Plan.from_bytes(data)
+    assert _plan_sig(a) == _plan_sig(b)
+    assert (a.rows, a.cols, a.n_lossy, a.max_wr, a.max_wc) == (b.rows, b.cols, b.n_lossy, b.max_wr, b.max_wc)
+    with pytest.raises(ValueError, match="truncated"):
+        P.Plan.from_bytes(data[: len(data) // 2])
+    with pytest.raises(ValueError, match="not a serialised plan"):
+        P.Plan.from_bytes(b"\0" * len(data))

@@ -94,7 +94,11 @@ def _worker(rank, world, port, out):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     img, mask = _scene()
     params = _params()
-    plan = P.build_plan(mask, params)
+    # rank 0 plans, the others import the broadcast bytes (the GPU default)
+    plan = strips.broadcast_plan(mask, params, "optimized", rank, dist, None, 0)
+    local = P.build_plan(mask, params)
+    assert plan.batches() == local.batches() and plan.levels() == local.levels()
+    assert (plan.ranks() == local.ranks()).all() and plan.unconcealed() == local.unconcealed()
     R = strips.halo_rows(params)
     processed = (plan.ranks() != np.iinfo(np.int32).max).reshape(plan.rows, plan.cols)
     bands = strips.band_partition(processed.sum(axis=1), world, R)
