@@ -443,6 +443,9 @@ struct MinBarrier {
     }
 };
 
+#ifndef FSE_PLAN_SOLO  // dev knob: solo threshold (band candidates at N_min); -1 = never
+#define FSE_PLAN_SOLO 4
+#endif
 template <typename CT, typename HT>
 struct BandPlanner {
     const Geometry &G;
@@ -463,6 +466,7 @@ struct BandPlanner {
         int r0 = 0, r1 = 0, base = 0, nblk = 0;
         uint32_t epoch = 0;                // barrier epochs passed
         std::vector<uint64_t> bits, summ;  // [word][count], summary [sword][count]
+        std::vector<uint64_t> supr;        // [sword / 64][count]: non-empty summary words
         std::vector<long> bsize;
         std::vector<int32_t> sel, prev_ok, okb, okptr, deferred, rowbuf;
         std::vector<uint8_t> lastrow;  // own last row's taken flags after the speculative select
@@ -478,6 +482,9 @@ struct BandPlanner {
     std::atomic<int> any_lastchanged{0};
     std::atomic<int> overflow{0};  // a level does not fit HT: the caller re-plans with int32
     int n_phases = 0;
+    int solo_next = 0;  // phase after thread 0's solo stretch (read after the park barrier)
+    // phases whose bands hold at most this many candidates each run solo
+    static constexpr int kSoloMax = FSE_PLAN_SOLO;
     bool prof = false;
 
     BandPlanner(const Geometry &G_, int T_, int R_, int NC_, const std::vector<int> &s_, CT *cnt_, const Usable &u,
@@ -492,14 +499,41 @@ struct BandPlanner {
         const int l = b - bd.base;
         bd.bits[(size_t)(l >> 6) * NC + c] |= 1ull << (l & 63);
         bd.summ[(size_t)(l >> 12) * NC + c] |= 1ull << ((l >> 6) & 63);
+        bd.supr[(size_t)(l >> 18) * NC + c] |= 1ull << ((l >> 12) & 63);
         ++bd.bsize[c];
     }
     void del(Band &bd, int c, int b) {
         const int l = b - bd.base;
         uint64_t &w = bd.bits[(size_t)(l >> 6) * NC + c];
         w &= ~(1ull << (l & 63));
-        if (!w) bd.summ[(size_t)(l >> 12) * NC + c] &= ~(1ull << ((l >> 6) & 63));
+        if (!w) {
+            uint64_t &sw = bd.summ[(size_t)(l >> 12) * NC + c];
+            sw &= ~(1ull << ((l >> 6) & 63));
+            if (!sw) bd.supr[(size_t)(l >> 18) * NC + c] &= ~(1ull << ((l >> 12) & 63));
+        }
         --bd.bsize[c];
+    }
+    // blocks of bucket c of band bd in ascending order, through the two summary levels
+    template <class Fn>
+    void scan_bucket(const Band &bd, int c, Fn &&fn) const {
+        const int nsup = (int)(bd.supr.size() / NC);
+        for (int u = 0; u < nsup; ++u) {
+            uint64_t su = bd.supr[(size_t)u * NC + c];
+            while (su) {
+                const int sw = (u << 6) + __builtin_ctzll(su);
+                su &= su - 1;
+                uint64_t sm = bd.summ[(size_t)sw * NC + c];
+                while (sm) {
+                    const int w = (sw << 6) + __builtin_ctzll(sm);
+                    sm &= sm - 1;
+                    uint64_t m = bd.bits[(size_t)w * NC + c];
+                    while (m) {
+                        fn(bd.base + (w << 6) + __builtin_ctzll(m));
+                        m &= m - 1;
+                    }
+                }
+            }
+        }
     }
     // blocks of bucket c in the global block range [lo, hi) of band bd, ascending
     template <class Fn>
@@ -525,6 +559,7 @@ struct BandPlanner {
         const int words = (bd.nblk + 63) / 64, swords = (words + 63) / 64;
         bd.bits.assign((size_t)words * NC, 0);
         bd.summ.assign((size_t)swords * NC, 0);
+        bd.supr.assign((size_t)((swords + 63) / 64) * NC, 0);
         bd.bsize.assign(NC, 0);
         bd.lastrow.assign(cols, 0);
         bd.okptr.assign(1, 0);
@@ -604,6 +639,81 @@ struct BandPlanner {
         bd.prev_ok.clear();
     }
 
+    int owner_band(int r) const { return (int)(std::upper_bound(s.begin(), s.end(), r) - s.begin()) - 1; }
+
+    // degeneracy, rank and level of band bd's members of phase ph
+    // (conceal.py:145-163), in row-major order
+    void finish_members(Band &bd, int ph) {
+        for (int b : bd.sel) {
+            if (!usable(b)) {
+                bd.deferred.push_back(b);
+                continue;
+            }
+            rank[b] = ph;
+            const int r = b / cols, c = b - r * cols;
+            int m = -1;
+            for (int rr = std::max(0, r - R); rr <= std::min(rows - 1, r + R); ++rr)
+                m = std::max(m, (int)HL[(size_t)rr * cols + c]);
+            level[b] = m + 1;
+            bd.maxlev = std::max(bd.maxlev, m + 1);
+            if (m + 1 >= (int)std::numeric_limits<HT>::max()) overflow.store(1, std::memory_order_relaxed);
+            bd.okb.push_back(b);
+            bd.prev_ok.push_back(b);
+        }
+        bd.okptr.push_back((int32_t)bd.okb.size());
+    }
+
+    // smallest pending count over every band, and the largest band's number of
+    // pending blocks at it (the solo test); kNone when nothing is pending
+    int global_min(int &maxcand) const {
+        int nm = kNone;
+        for (const Band &o : bands)
+            for (int c = 0; c < std::min(nm, NC); ++c)
+                if (o.bsize[c]) {
+                    nm = c;
+                    break;
+                }
+        maxcand = 0;
+        if (nm != kNone)
+            for (const Band &o : bands) maxcand = std::max(maxcand, (int)o.bsize[nm]);
+        return nm;
+    }
+
+    // One whole phase on thread 0 while the other band threads are parked:
+    // select_batch over all rows in order, then commit_batch, degeneracy and
+    // levels.  Used for the phases whose N_min bucket is tiny (most phases of
+    // a large frame hold a handful of blocks): no synchronisation at all.
+    void solo_phase(int ph, int nmin) {
+        for (Band &o : bands) o.sel.clear();
+        for (Band &o : bands) {
+            if (!o.bsize[nmin]) continue;
+            scan_bucket(o, nmin, [&](int b) {
+                const int r = b / cols, c = b - r * cols;
+                if (c > 0 && cnt[b - 1] == kTaken) return;
+                if (r > 0) {
+                    const int up = b - cols;
+                    if (cnt[up] == kTaken || (c > 0 && cnt[up - 1] == kTaken) ||
+                        (c + 1 < cols && cnt[up + 1] == kTaken))
+                        return;
+                }
+                cnt[b] = kTaken;
+                o.sel.push_back(b);
+            });
+        }
+        for (Band &o : bands)
+            for (int b : o.sel) {
+                del(o, nmin, b);
+                cnt[b] = -1;
+            }
+        for (Band &o : bands)
+            for (int b : o.sel) {
+                const int r = b / cols;
+                const int q0 = owner_band(std::max(0, r - 1)), q1 = owner_band(std::min(rows - 1, r + 1));
+                for (int q = q0; q <= q1; ++q) release_around(bands[q], b, bands[q].r0, bands[q].r1);
+            }
+        for (Band &o : bands) finish_members(o, ph);
+    }
+
     void run(int k) {
         Band &bd = bands[k];
         init_band(k);
@@ -616,21 +726,46 @@ struct BandPlanner {
             tp = n;
         };
         for (int ph = 0;; ++ph) {
-            // ---- A: the phase's N_min
+            // ---- A: the phase's N_min, and the largest band candidate count at
+            // it (packed: count 0xFFFF - n in the low bits, so min picks it)
             int lm = kNone;
             for (int c = 0; c < NC; ++c)
                 if (bd.bsize[c]) {
                     lm = c;
                     break;
                 }
+            const int key = lm == kNone ? kNone : (lm << 16) | (0xFFFF - (int)std::min<long>(bd.bsize[lm], 0xFFFF));
             lapt(bd.com_ms);
-            const int nmin = sync_min(k, lm);
+            const int red = sync_min(k, key);
             lapt(bd.wait_ms);
-            apply_prev(bd);
-            if (nmin == kNone) {
+            if (red == kNone) {
+                apply_prev(bd);
                 if (k == 0) n_phases = ph;
                 break;
             }
+            const int nmin = red >> 16, maxcand = 0xFFFF - (red & 0xFFFF);
+            if (maxcand <= kSoloMax) {
+                // ---- a stretch of tiny phases on thread 0; the others park.
+                // Thread 0 also applies every band's previous-phase results
+                // (the owners skip it here, so nothing races its level queries)
+                if (k == 0) {
+                    int p = ph, nm = nmin, mc = maxcand;
+                    for (;;) {
+                        for (Band &o : bands) apply_prev(o);  // results of phase p - 1
+                        solo_phase(p, nm);
+                        ++p;
+                        nm = global_min(mc);
+                        if (nm == kNone || mc > kSoloMax) break;
+                    }
+                    solo_next = p;
+                    lapt(bd.sel_ms);
+                }
+                sync_min(k, 0);
+                lapt(bd.wait_ms);
+                ph = solo_next - 1;
+                continue;
+            }
+            apply_prev(bd);
             // ---- speculative select (select_batch, schedule.py:60-82)
             bd.sel.clear();
             bd.lastchanged = false;
@@ -714,23 +849,7 @@ struct BandPlanner {
                 for (size_t i = 0; i < sl.size() && sl[i] < lim; ++i) release_around(bd, sl[i], bd.r0, bd.r1);
             }
             // ---- snapshot + degeneracy (conceal.py:145-163) and level queries
-            for (int b : bd.sel) {
-                if (!usable(b)) {
-                    bd.deferred.push_back(b);
-                    continue;
-                }
-                rank[b] = ph;
-                const int r = b / cols, c = b - r * cols;
-                int m = -1;
-                for (int rr = std::max(0, r - R); rr <= std::min(rows - 1, r + R); ++rr)
-                    m = std::max(m, (int)HL[(size_t)rr * cols + c]);
-                level[b] = m + 1;
-                bd.maxlev = std::max(bd.maxlev, m + 1);
-                if (m + 1 >= (int)std::numeric_limits<HT>::max()) overflow.store(1, std::memory_order_relaxed);
-                bd.okb.push_back(b);
-                bd.prev_ok.push_back(b);
-            }
-            bd.okptr.push_back((int32_t)bd.okb.size());
+            finish_members(bd, ph);
         }
     }
 };
