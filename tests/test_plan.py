@@ -416,3 +416,20 @@ def test_plan_export_import_round_trip_and_rejects_corrupt_bytes():
         P.Plan.from_bytes(data[: len(data) // 2])
     with pytest.raises(ValueError, match="not a serialised plan"):
         P.Plan.from_bytes(b"\0" * len(data))
+
+
+@pytest.mark.parametrize("shape,B,fill", [((1, 200), 1, 1.0), ((300, 1), 1, 0.7), ((64, 64), 4, 1.0),
+                                          ((64, 64), 4, 0.0), ((96, 40), 2, 0.97), ((17, 300), 3, 0.5)])
+def test_band_parallel_planner_edge_grids(shape, B, fill):
+    """Degenerate grids for the band-parallel planner: one block row or column,
+    everything lost (every window degenerate: all blocks unconcealed), nothing
+    lost, almost everything lost -- identical to the sequential planner for
+    every thread count."""
+    rng = np.random.default_rng(int(fill * 100) + shape[0])
+    mask = (rng.random(shape) < fill).astype(np.uint8)
+    for delta in (0.0, 0.2):
+        p = P.FseParams(d=5, iterations=5, block_size=B, delta=delta)
+        ref = _plan_sig(P.build_plan(mask, p, plan_threads=1))
+        rows = -(-shape[0] // B)
+        for T in (2, 3, 7, rows):
+            assert _plan_sig(P.build_plan(mask, p, plan_threads=T)) == ref, (T, delta)
