@@ -40,10 +40,10 @@ namespace fse {
 // dev instrumentation (-DFSE_CLOCKS): CTA 0, thread 0 records clock64() at the
 // phase boundaries of its window (fse_debug_clocks reads them back)
 #ifdef FSE_CLOCKS
-static __device__ long long g_fse_clk[1024];
+static __device__ long long g_fse_clk[1024 + 8];
 #define FSE_CLK(i)                                                               \
     do {                                                                         \
-        if (blockIdx.x == 0 && threadIdx.x == 0 && (i) < 1024) g_fse_clk[(i)] = clock64(); \
+        if (blockIdx.x == 0 && threadIdx.x == 0 && (i) < 1024 + 8) g_fse_clk[(i)] = clock64(); \
     } while (0)
 #else
 #define FSE_CLK(i) \
@@ -610,15 +610,8 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
 #endif
     constexpr bool TW_ROT = !IS_F32 && FSE_TW_ROT;
     const T2 trot = tw[tstep];  // e^{+j 2 pi 4 v0 / F}
-    auto partials = [&](const T2 *Y) {
-        // (-DFSE_PART_NOUNROLL halves the kernel's code: config 1 fp64 1.9 vs
-        // 2.0 ms, but config 4 fp32 +6%, fp64 +0.5%: unrolled by default)
-#ifdef FSE_PART_NOUNROLL
-#pragma unroll 1
-#else
-#pragma unroll
-#endif
-        for (int j = 0; j < NB; ++j) {
+    auto part_one = [&](const T2 *Y, int j) {
+        {
             const int u = u0 + RSTEP * j;
             if (u < R1) {
                 const T2 *yr = Y + u * N;
@@ -645,6 +638,26 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
                 part[(u * 4 + q4) * QW + v0] = acc;
             }
         }
+    };
+    auto partials = [&](const T2 *Y) {
+        // (-DFSE_PART_NOUNROLL halves the kernel's code: config 1 fp64 1.9 vs
+        // 2.0 ms, but config 4 fp32 +6%, fp64 +0.5%: unrolled by default)
+#ifdef FSE_PART_NOUNROLL
+#pragma unroll 1
+#else
+#pragma unroll
+#endif
+        for (int j = 0; j < NB; ++j) part_one(Y, j);
+    };
+    // the w pass runs while G is live in registers: rolled, it needs fewer
+    // of them (dev knob FSE_W_ROLLED)
+    auto partials_w = [&](const T2 *Y) {
+#if defined(FSE_W_ROLLED) && FSE_W_ROLLED
+#pragma unroll 1
+        for (int j = 0; j < NB; ++j) part_one(Y, j);
+#else
+        partials(Y);
+#endif
     };
     auto combine = [&](int u) -> T2 {
         const T2 *pr = part + (u * 4) * QW + v0;
@@ -675,8 +688,9 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     }
     __syncthreads();
     FSE_CLK(3);
-    partials(Yw);
+    partials_w(Yw);
     __syncthreads();
+    FSE_CLK(1000);
     // W half rows 0..F/2; with EXT (one CTA per window) also the negative
     // rows W[-u][-v] = conj W[u][v] at once: they land in the dead x/w/Y
     // staging bytes below the half rows, while `part` (above them) is still
@@ -719,6 +733,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         }
     }
     __syncthreads();
+    FSE_CLK(1001);
     if constexpr (!C::EXT && !C::HALF) {
         // plain plane: rows F/2+1 .. F-1 by W[r][c] = conj W[F-r][-c], and
         // row F = row 0 (the update's row u + a <= F then never wraps)

@@ -363,7 +363,7 @@ int fast_windows(int dtype, int F, const FastArgs &a, int grid, cudaStream_t s) 
 
 #ifdef FSE_CLOCKS
 extern "C" int fse_debug_clocks(long long *out, int n) {
-    return cudaMemcpyFromSymbol(out, fse::g_fse_clk, sizeof(long long) * (size_t)std::min(n, 1024)) == cudaSuccess
+    return cudaMemcpyFromSymbol(out, fse::g_fse_clk, sizeof(long long) * (size_t)std::min(n, 1032)) == cudaSuccess
                ? 0
                : -5;
 }

@@ -39,8 +39,8 @@ for prec in sys.argv[1:] or ["fp32", "fp64"]:
         work = src.clone()
         P.run_frames_device([plan], [work], [m], [mo], p, prec)
         torch.cuda.synchronize()
-    clk = np.zeros(1024, np.int64)
-    assert L.fse_debug_clocks(clk.ctypes.data, 1024) == 0
+    clk = np.zeros(1032, np.int64)
+    assert L.fse_debug_clocks(clk.ctypes.data, 1032) == 0
     c = clk
     it = np.array([c[8 + 4 * i: 12 + 4 * i] for i in range(100)])
     nxt = np.append(it[1:, 0], c[5])
@@ -49,7 +49,9 @@ for prec in sys.argv[1:] or ["fp32", "fp64"]:
            "update loop": np.median(nxt[10:90] - it[10:90, 2])}
     rec = {"precision": prec, "F": F, "windows": n, "variant": os.environ.get("FSE_F64L", "0"),
            "setup_cycles": {"twiddles+staging": int(c[1] - c[0]), "column pass": int(c[2] - c[1]),
-                            "x row pass": int(c[3] - c[2]), "w row pass + W plane": int(c[4] - c[3])},
+                            "x row pass": int(c[3] - c[2]), "w row pass + W plane": int(c[4] - c[3]),
+                            "(w partials)": int(c[1000] - c[3]), "(w combine)": int(c[1001] - c[1000]),
+                            "(W mirror rows)": int(c[4] - c[1001])},
            "loop_cycles": int(c[5] - c[4]), "writeback_cycles": int(c[6] - c[5]),
            "per_iteration_cycles": {k: float(v) for k, v in seg.items()}}
     print(json.dumps(rec), flush=True)
