@@ -145,7 +145,10 @@ template <typename T> using Fast128 = FastCfg<T, 128, FSE_F128_NW>;
 using Fast128T = FastCfg<float, 128, FSE_F128T_NW, true, 0, 1, true>;
 #ifdef FSE_WITH_CLUSTER  // experiment, measured slower everywhere: not in the default build
 // Cluster variants for levels narrower than the GPU: one window over CL SMs.
-template <typename T, int CL> using Fast64C = FastCfg<T, 64, 6, sizeof(T) == 4, 0, CL>;
+#ifndef FSE_CL_NW  // dev knob: warps per CTA of the F = 64 cluster variants
+#define FSE_CL_NW 6
+#endif
+template <typename T, int CL> using Fast64C = FastCfg<T, 64, (FSE_CL_NW < 32 / CL ? FSE_CL_NW : 32 / CL), sizeof(T) == 4, 0, CL>;
 template <typename T, int CL> using Fast32C = FastCfg<T, 32, 6, true, 0, CL>;
 
 // FSE_CLUSTER: unset / 0 = off (default), 2 / 4 = that cluster size, -1 = automatic.
