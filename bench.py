@@ -403,6 +403,7 @@ def run_b200(a, rank, world, local_rank):
         lib.fse_launch_count(1)
         lib.fse_timing_read(None, None, None)
         lib.fse_guard_redo_count(1)
+        lib.fse_wcache_stats(None, None, None, 1)
         lib.fse_timing_enable(1)
         clk = ClockSampler(local_rank) if sample_clocks else None
         if clk:
@@ -415,7 +416,12 @@ def run_b200(a, rank, world, local_rank):
         kms, wl, calls = ctypes.c_double(), ctypes.c_int64(), ctypes.c_int64()
         _lib.check(lib.fse_timing_read(ctypes.byref(kms), ctypes.byref(wl), ctypes.byref(calls)))
         redo = int(lib.fse_guard_redo_count(1))
-        return {"ms": ms, "kernel_ms": kms.value / a.steps, "launches": launches,
+        wcw, wch, wcp = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        lib.fse_wcache_stats(ctypes.byref(wcw), ctypes.byref(wch), ctypes.byref(wcp), 1)
+        wcache = {"windows_per_step": wcw.value / a.steps, "hits_per_step": wch.value / a.steps,
+                  "planes_per_step": wcp.value / a.steps,
+                  "hit_share": (wch.value / wcw.value) if wcw.value else 0.0}
+        return {"ms": ms, "kernel_ms": kms.value / a.steps, "launches": launches, "wcache": wcache,
                 "level_launches": int(wl.value),
                 "plan_ms": float(np.mean(plan_ms)) if plan_ms else None, "redo": redo / a.steps,
                 "clocks": clk.summary() if clk else None}
@@ -524,6 +530,7 @@ def run_b200(a, rank, world, local_rank):
             "host_enqueue_ms_per_step": head["plan_ms"],
             "kernel_ms_per_step": head["kernel_ms"],
             "fp32_guard_fp64_redo_per_step": head["redo"],
+            "weight_spectrum_cache": head["wcache"],
             "parity": PARITY[a.precision],
             "roofline": roof(head, a.precision),
             "gpu_launches": head["launches"],

@@ -175,6 +175,19 @@ int fse_set_dataflow(int32_t on);
  * another group's work.  1..8, default 2 (FSE_GROUPS sets the default).
  * Results are identical for every n.  Process-wide. */
 int fse_set_groups(int32_t n);
+/* Weight-spectrum cache of a session (fast path): W = fft2(w) of
+ * _kernel.pyx:148 depends only on a window's shape and class map
+ * (fse.py:105-119), so windows of one call that share both share W.  1
+ * (default; FSE_WCACHE=0 sets the default off): before the first level every
+ * window's class map is hashed and compared on the device, each W shared by
+ * >= 2 windows is computed once, and the level kernels load it instead of
+ * running the weight half of their set-up.  Results are bit-identical to 0
+ * (every window computes its own W).  Process-wide. */
+int fse_set_wcache(int32_t on);
+/* Totals over the sessions read back by fse_timing_read so far: windows
+ * classified, windows that loaded a cached W, planes wanted (distinct shared
+ * maps; may exceed the plane capacity).  reset != 0 clears them. */
+int fse_wcache_stats(int64_t *windows, int64_t *hits, int64_t *planes, int32_t reset);
 /* fp32 argmax form per level launch: launches of fewer windows than this use
  * the tracked argmax (each thread carries its best bin; one barrier per
  * iteration), wider ones the lazy argmax (running maximum only; the winning

@@ -23,6 +23,7 @@ EXPORTS = (
     "fse_plan_unconcealed", "fse_plan_export_size", "fse_plan_export", "fse_plan_import", "fse_init_counts", "fse_schedule_all", "fse_conceal_frames",
     "fse_launch_count", "fse_timing_enable", "fse_timing_read", "fse_fma_probe",
     "fse_set_guard", "fse_guard_redo_count", "fse_set_dataflow", "fse_set_groups", "fse_set_track_below",
+    "fse_set_wcache", "fse_wcache_stats",
     "fse_shard_open", "fse_shard_levels", "fse_shard_run", "fse_shard_close",
     "fse_ipc_handle", "fse_ipc_open", "fse_ipc_close", "fse_flags_alloc", "fse_flags_free",
     "fse_shard_set_peers", "fse_quantize_psnr",
@@ -103,6 +104,9 @@ def lib():
         L.fse_set_dataflow.argtypes = [_i32]
         L.fse_set_groups.argtypes = [_i32]
         L.fse_set_track_below.argtypes = [_i32]
+        L.fse_set_wcache.argtypes = [_i32]
+        _pi64 = ctypes.POINTER(ctypes.c_int64)
+        L.fse_wcache_stats.argtypes = [_pi64, _pi64, _pi64, _i32]
         L.fse_shard_open.argtypes = [_vp, _i32, _i32, _vp, _vp, _vp, ctypes.POINTER(FseParamsC), _i32,
                                      _vp, _i32, _vp, ctypes.POINTER(_vp)]
         L.fse_shard_levels.argtypes = [_vp, _pi32, _pi32]

@@ -30,7 +30,7 @@ if _TAG:
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
               "--expt-relaxed-constexpr"]
-HEADERS = ["fse_fit.cuh", "fse_common.h", "fse_kernel.cuh", "fse_fast.cuh", "fse_gen.cuh"]
+HEADERS = ["fse_fit.cuh", "fse_common.h", "fse_kernel.cuh", "fse_fast.cuh", "fse_gen.cuh", "fse_wcache.h"]
 
 
 def _nvcc() -> str:

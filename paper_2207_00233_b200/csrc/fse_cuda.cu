@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 
 #include <algorithm>
 #include <mutex>
@@ -14,6 +16,7 @@
 
 #include "fse_fast.cuh"
 #include "fse_gen.cuh"
+#include "fse_wcache.h"
 
 namespace fse {
 
@@ -27,6 +30,8 @@ struct TimingState {
     long long window_launches = 0;
     // per-call guard counters copied back asynchronously (pinned), summed on read
     std::vector<std::pair<int *, int>> redo;
+    // per-session W-cache counters (planes wanted, hits) copied back likewise, with the session's windows
+    std::vector<std::pair<int *, long long>> wc;
 };
 static thread_local TimingState g_timing;
 
@@ -53,6 +58,25 @@ static std::atomic<int> g_groups{[] {
     const int v = e ? atoi(e) : 2;
     return std::max(1, std::min(v, 8));
 }()};
+
+// Weight-spectrum cache of a session (fse_wcache.cu): windows that share their
+// shape and class map share W = DFT(w); each W shared by at least two windows
+// (FSE_WCACHE_MIN=1: every W) is computed once before the first level, up
+// to FSE_WCACHE_PLANES planes (default 65536) and FSE_WCACHE_MB of them (default
+// 4096), and the level kernels load it
+// from L2 instead of running the w half of the set-up.  On for sessions of at
+// least FSE_WCACHE_ENTRIES windows (default 2048: below that the three
+// classification launches cost more than they save).  FSE_WCACHE=0 or
+// fse_set_wcache(0) turns it off; results are bit-identical either way.
+static std::atomic<int> g_wcache{[] {
+    const char *e = getenv("FSE_WCACHE");
+    return e ? atoi(e) : 1;
+}()};
+static int env_int(const char *name, int dflt) {
+    const char *e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+static std::atomic<long long> g_wc_entries{0}, g_wc_hits{0}, g_wc_planes{0};
 
 // Pinned host staging buffers for the session uploads (frame table, ranks,
 // level entry lists; tens of MB for a 64-frame batch).  A pageable source
@@ -329,6 +353,12 @@ int fse_timing_read(double *ms, int64_t *window_launches, int64_t *calls) {
         cudaFreeHost(r.first);
     }
     fse::g_timing.redo.clear();
+    for (auto &r : fse::g_timing.wc) {
+        fse::g_wc_entries += r.second;
+        fse::g_wc_planes += r.first[0];
+        fse::g_wc_hits += r.first[1];
+    }
+    fse::g_timing.wc.clear();
     if (ms) *ms = tot;
     if (window_launches) *window_launches = fse::g_timing.window_launches;
     if (calls) *calls = n;
@@ -392,6 +422,23 @@ int fse_set_dataflow(int32_t on) {
 int fse_set_track_below(int32_t windows) {
     if (windows < 0) return fail(FSE_EINVAL, "track_below must be >= 0");
     fse::g_track_below.store(windows, std::memory_order_relaxed);
+    return FSE_OK;
+}
+
+int fse_set_wcache(int32_t on) {
+    fse::g_wcache.store(on ? 1 : 0);
+    return FSE_OK;
+}
+
+int fse_wcache_stats(int64_t *windows, int64_t *hits, int64_t *planes, int32_t reset) {
+    if (windows) *windows = fse::g_wc_entries.load();
+    if (hits) *hits = fse::g_wc_hits.load();
+    if (planes) *planes = fse::g_wc_planes.load();
+    if (reset) {
+        fse::g_wc_entries = 0;
+        fse::g_wc_hits = 0;
+        fse::g_wc_planes = 0;
+    }
     return FSE_OK;
 }
 
@@ -477,6 +524,9 @@ struct FseShard {
     std::vector<int32_t> need_up, need_down;
     unsigned char *dev = nullptr;
     size_t off_ent = 0, off_cnt = 0, off_next = 0, off_done = 0, off_queue = 0, off_redo = 0;
+    // weight-spectrum cache (0 planes = off): per-entry plane index, counters
+    size_t off_wslot = 0, off_wcnt = 0;
+    int wc_cap = 0;
     bool fast = false, guard = false, masks_out = false;
     fse::KArgs a{};
     fse::FastArgs f{};
@@ -613,14 +663,70 @@ static int session_open(int32_t n, FsePlan *const *plans, void *const *images, c
     S->off_done = S->off_next + 256;
     S->off_queue = S->off_done + up256(sizeof(int) * (size_t)nb * n);
     S->off_redo = S->off_queue + up256(sizeof(int) * std::max<size_t>(n_entries, 1));
-    const size_t bytes = S->off_redo + sizeof(int2) * std::max<size_t>(n_entries, 1);
+    size_t bytes = S->off_redo + sizeof(int2) * std::max<size_t>(n_entries, 1);
+    // weight-spectrum cache regions (after everything else):
+    //   zeroed: counters | table keys | table counts;  0xFF: representatives;
+    //   scratch: plane of each slot | slot of each entry | plane of each entry |
+    //   representative of each plane | signatures | planes
+    const bool fast_session = F1 == F2 && F1 && fast_supported(dtype, F1, S->Mmax, S->Nmax, S->model_n, p->iterations);
+    const bool guard_session = fast_session && dtype == FSE_F32 && g_tau0 >= 0.0 && F1 != 128;
+    WCacheArgs wa{};
+    size_t off_wkeys = 0, off_wrepslot = 0, off_wzero_end = 0, off_wff_end = 0, off_planes = 0;
+    // F >= 64 by default: at F = 32 (config 5, B = 2) the set-up is too small a
+    // share of a window for the classification to pay (measured 180 vs 172 ms)
+    if (fast_session && !guard_session && g_wcache.load() > 0 && !dataflow_enabled() &&
+        F1 >= env_int("FSE_WCACHE_MIN_F", 64) &&
+        n_entries >= (size_t)std::max(1, env_int("FSE_WCACHE_ENTRIES", 2048)) && n_entries < ((size_t)1 << 30)) {
+        const size_t elem = 2 * (dtype == FSE_F64 ? sizeof(double) : sizeof(float));
+        const size_t plane_bytes = (size_t)(F1 / 2 + 1) * F1 * elem;
+        wa.min_count = std::max(1, env_int("FSE_WCACHE_MIN", 2));
+        // (a plane serves >= 2 windows, so n / 2 planes are enough)
+        S->wc_cap = (int)std::min<size_t>(std::max<size_t>(wa.min_count > 1 ? n_entries / 2 : n_entries, 1),
+                                          (size_t)std::max(1, env_int("FSE_WCACHE_PLANES", 65536)));
+        // and at most FSE_WCACHE_MB of planes (default 4 GiB: 127 k planes at fp64 F = 64, 31 k at F = 128)
+        S->wc_cap = (int)std::max<size_t>(1, std::min<size_t>((size_t)S->wc_cap,
+                                                              ((size_t)std::max(1, env_int("FSE_WCACHE_MB", 4096)) << 20) / plane_bytes));
+        size_t slots = 1024;
+        while (slots < 2 * n_entries) slots <<= 1;
+        wa.tmask = (uint32_t)(slots - 1);
+        wa.SW = 1 + S->Mmax * ((S->Nmax + 31) / 32);
+        wa.cap = S->wc_cap;
+        wa.n_entries = (int)n_entries;
+        S->off_wcnt = up256(bytes);
+        off_wkeys = S->off_wcnt + 256;
+        const size_t off_wtcnt = off_wkeys + up256(sizeof(unsigned long long) * slots);
+        off_wzero_end = off_wtcnt + up256(sizeof(uint32_t) * slots);
+        off_wrepslot = off_wzero_end;
+        off_wff_end = off_wrepslot + up256(sizeof(uint32_t) * slots);
+        const size_t off_cidx = off_wff_end;
+        const size_t off_slotof = off_cidx + up256(sizeof(int32_t) * slots);
+        S->off_wslot = off_slotof + up256(sizeof(int32_t) * n_entries);
+        const size_t off_wrep = S->off_wslot + up256(sizeof(int32_t) * n_entries);
+        const size_t off_sig = off_wrep + up256(sizeof(int32_t) * (size_t)S->wc_cap);
+        off_planes = off_sig + up256(sizeof(unsigned long long) * n_entries * (size_t)wa.SW);
+        bytes = off_planes + plane_bytes * (size_t)S->wc_cap;
+        // offsets into pointers once the buffer exists (below)
+        wa.counters = reinterpret_cast<int *>(S->off_wcnt);
+        wa.keys = reinterpret_cast<unsigned long long *>(off_wkeys);
+        wa.cnt = reinterpret_cast<uint32_t *>(off_wtcnt);
+        wa.rep = reinterpret_cast<uint32_t *>(off_wrepslot);
+        wa.cidx = reinterpret_cast<int32_t *>(off_cidx);
+        wa.slot_of = reinterpret_cast<int32_t *>(off_slotof);
+        wa.wslot = reinterpret_cast<int32_t *>(S->off_wslot);
+        wa.wrep = reinterpret_cast<int32_t *>(off_wrep);
+        wa.sig = reinterpret_cast<unsigned long long *>(off_sig);
+    }
     int slot = -1;
     unsigned char *host = nullptr;
     if (int rc = stage_acquire(S->off_cnt, &slot, &host)) {
         delete S;
         return rc;
     }
+    // dev: FSE_OPEN_TIMING=1 prints the host time of the staging allocation and of the whole open
+    static const bool open_timing = env_int("FSE_OPEN_TIMING", 0) != 0;
+    const auto t_open0 = std::chrono::steady_clock::now();
     cudaError_t ce = staging_alloc((void **)&S->dev, bytes, s);
+    const auto t_open1 = std::chrono::steady_clock::now();
     if (ce != cudaSuccess) {
         stage_release(slot, s);
         delete S;
@@ -653,6 +759,10 @@ static int session_open(int32_t n, FsePlan *const *plans, void *const *images, c
     stage_release(slot, s);
     if (ce == cudaSuccess) ce = cudaMemsetAsync(dev + S->off_cnt, 0, S->off_queue - S->off_cnt, s);
     if (ce == cudaSuccess) ce = cudaMemsetAsync(dev + S->off_queue, 0xFF, S->off_redo - S->off_queue, s);
+    if (ce == cudaSuccess && S->wc_cap > 0) {
+        ce = cudaMemsetAsync(dev + S->off_wcnt, 0, off_wzero_end - S->off_wcnt, s);
+        if (ce == cudaSuccess) ce = cudaMemsetAsync(dev + off_wrepslot, 0xFF, off_wff_end - off_wrepslot, s);
+    }
     if (ce != cudaSuccess) {
         cudaFreeAsync(dev, s);
         delete S;
@@ -694,6 +804,68 @@ static int session_open(int32_t n, FsePlan *const *plans, void *const *images, c
         f.tau0 = (float)g_tau0.load();
         f.tau1 = (float)g_tau1.load();
         f.R = S->R;
+    }
+    if (S->wc_cap > 0) {
+        // classify every window of the session, then compute each shared W once
+        auto at = [&](auto *off) { return reinterpret_cast<decltype(off)>(dev + reinterpret_cast<size_t>(off)); };
+        wa.frames = a.frames;
+        wa.entries = reinterpret_cast<const int2 *>(dev + S->off_ent);
+        wa.H = a.H; wa.W = a.W; wa.B = a.B; wa.d = a.d; wa.rows = a.rows; wa.cols = a.cols;
+        wa.counters = at(wa.counters);
+        wa.keys = at(wa.keys);
+        wa.cnt = at(wa.cnt);
+        wa.rep = at(wa.rep);
+        wa.cidx = at(wa.cidx);
+        wa.slot_of = at(wa.slot_of);
+        wa.wslot = at(wa.wslot);
+        wa.wrep = at(wa.wrep);
+        wa.sig = at(wa.sig);
+        cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+        if (g_timing.on && cudaEventCreate(&ev0) == cudaSuccess && cudaEventCreate(&ev1) == cudaSuccess)
+            cudaEventRecord(ev0, s);
+        int rc = wcache_classify(wa, s);
+        if (rc == FSE_OK) {
+            FastArgs &f = S->f;
+            f.wplanes = dev + off_planes;
+            f.wrep = wa.wrep;
+            FastArgs pr = f;
+            pr.entries = wa.entries;
+            pr.count = wa.counters;
+            pr.picks = nullptr;
+            rc = fast_wplanes(dtype, F1, pr, S->wc_cap, S->Mmax, S->Nmax, S->model_n, s);
+        }
+        if (rc != FSE_OK) {
+            cudaFreeAsync(dev, s);
+            delete S;
+            return rc;
+        }
+        if (ev0 && ev1) {
+            // the pre-pass counts towards the kernel time bench.py reports
+            cudaEventRecord(ev1, s);
+            g_timing.ev.emplace_back(ev0, ev1);
+        }
+        if (g_timing.on) {
+            // counters into a slot of a pinned ring allocated once per thread
+            // (a cudaMallocHost per session stalls the launching thread)
+            static thread_local int *ring = nullptr;
+            static thread_local unsigned ring_pos = 0;
+            constexpr unsigned kRing = 256;
+            if (!ring && cudaMallocHost((void **)&ring, sizeof(int) * 2 * kRing) != cudaSuccess) {
+                ring = nullptr;
+                cudaGetLastError();
+            }
+            if (ring && g_timing.wc.size() < kRing) {
+                int *hc = ring + 2 * (ring_pos++ % kRing);
+                cudaMemcpyAsync(hc, wa.counters, sizeof(int) * 2, cudaMemcpyDeviceToHost, s);
+                g_timing.wc.emplace_back(hc, (long long)n_entries);
+            }
+        }
+    }
+    if (open_timing) {
+        const auto t_open2 = std::chrono::steady_clock::now();
+        fprintf(stderr, "fse session_open: %d frames, %zu entries, %.1f MB staged: alloc %.3f ms, rest %.3f ms\n", n,
+                n_entries, bytes / 1e6, std::chrono::duration<double, std::milli>(t_open1 - t_open0).count(),
+                std::chrono::duration<double, std::milli>(t_open2 - t_open1).count());
     }
     *out = S;
     return FSE_OK;
@@ -778,6 +950,7 @@ static int session_run(FseShard *S, int l0, int l1, bool whole, cudaStream_t s) 
     if (whole && S->fast && !S->guard && dataflow_enabled()) {
         // one persistent launch over all levels of all frames (fse_fast.cuh)
         f.entries = reinterpret_cast<const int2 *>(dev + S->off_ent);
+        f.wslot = nullptr;
         f.total = (int)S->n_entries;
         f.next = reinterpret_cast<int *>(dev + S->off_next);
         f.done = reinterpret_cast<int *>(dev + S->off_done);
@@ -838,6 +1011,7 @@ static int session_run(FseShard *S, int l0, int l1, bool whole, cudaStream_t s) 
                 f.entries = lvl;
                 f.redo_list = redo + S->lvl_off[l];
                 f.redo_count = counters + l;
+                f.wslot = S->wc_cap > 0 ? reinterpret_cast<const int32_t *>(dev + S->off_wslot) + S->lvl_off[l] : nullptr;
                 rc = fast_level(S->dtype, S->F1, false, f, cnt, S->Mmax, S->Nmax, S->model_n, s);
                 if (g_timing.on) ++g_timing.window_launches;
             }
@@ -865,9 +1039,11 @@ static int session_run(FseShard *S, int l0, int l1, bool whole, cudaStream_t s) 
                 f.entries = lvl;
                 f.redo_list = redo + S->lvl_off[q];
                 f.redo_count = counters + q;
+                f.wslot = S->wc_cap > 0 ? reinterpret_cast<const int32_t *>(dev + S->off_wslot) + S->lvl_off[q] : nullptr;
                 rc = fast_level(S->dtype, S->F1, S->guard, f, cnt, S->Mmax, S->Nmax, S->model_n, sg);
                 if (rc == FSE_OK && S->guard) {
                     FastArgs r = f;
+                    r.wslot = nullptr;
                     r.entries = redo + S->lvl_off[q];
                     r.count = counters + q;
                     rc = fast_redo(S->F1, r, cnt, S->Mmax, S->Nmax, S->model_n, sg);
@@ -939,11 +1115,21 @@ int fse_conceal_frames(int32_t n, FsePlan *const *plans, void *const *images,
     FseShard *S = nullptr;
     // the dataflow executor walks one level-ordered list: one group
     const int groups = fse::dataflow_enabled() ? 1 : fse::g_groups.load();
+    static const bool call_timing = fse::env_int("FSE_OPEN_TIMING", 0) != 0;
+    const auto t0 = std::chrono::steady_clock::now();
     int rc = fse::session_open(n, plans, images, masks, masks_out, p, dtype, decay, decay_dim, picks, 0,
                                plans[0]->p.rows, groups, s, &S);
     if (rc) return rc;
+    const auto t1 = std::chrono::steady_clock::now();
     rc = fse::session_run(S, 0, S->n_levels, true, s);
+    const auto t2 = std::chrono::steady_clock::now();
     const int rc2 = fse::session_close(S, rc == FSE_OK, s);
+    if (call_timing) {
+        const auto t3 = std::chrono::steady_clock::now();
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        fprintf(stderr, "fse_conceal_frames: %d frames: open %.3f ms, run %.3f ms, close %.3f ms\n", n, ms(t0, t1),
+                ms(t1, t2), ms(t2, t3));
+    }
     return rc ? rc : rc2;
 }
 

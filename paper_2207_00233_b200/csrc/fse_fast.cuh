@@ -239,6 +239,15 @@ struct FastArgs {
     // read.  nullptr = no neighbour on that side.
     void *peer_up, *peer_down;
     int peer_up_end, peer_down_begin;
+    // weight-spectrum cache (fse_wcache.cu): W = DFT(w) depends only on a
+    // window's shape and class map, not on image values, so windows of one
+    // session that share both share W.  wslot[entry] = plane index or -1;
+    // wplanes = planes of R1 x F complex (the half rows 0..F/2), written by
+    // the MODE 2 launch (one CTA per plane: entry wrep[plane] of `entries`,
+    // planes [0, *count)) before the first level.
+    const int32_t *wslot;
+    void *wplanes;
+    const int32_t *wrep;
 };
 
 __device__ __forceinline__ unsigned warp_max_u32(unsigned v) { return __reduce_max_sync(0xffffffffu, v); }
@@ -377,9 +386,13 @@ __device__ __forceinline__ T2 dft_mac(T2 acc, T2 z, T2 tw) {
     return cfma(T2{z.y, -z.x}, T2{tw.y, tw.y}, acc);
 }
 
-template <class C, int MODE, bool GUARD, typename IT>
+// WC: this window's W half rows are read from the session's cache plane `wc`
+// instead of being computed.  A compile-time flag, so the computing path keeps
+// exactly the code (and ptxas schedule) it has without the cache: a run-time
+// flag through the set-up cost the fp64 kernel 3.5% on config 4.
+template <class C, int MODE, bool GUARD, typename IT, bool WC = false>
 __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout &L, const int entry_idx,
-                                            unsigned char *sm, int2 entry_in = make_int2(-1, -1)) {
+                                            unsigned char *sm, int2 entry_in = make_int2(-1, -1), int wc = -1) {
     using T = typename C::T;
     using T2 = typename C::T2;
     constexpr int F = C::F, NW = C::NW, NT = C::NT, NB = C::NB, R1 = C::R1, SEG = C::SEG;
@@ -407,8 +420,17 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     int M, N, br0 = 0, bc0 = 0, bh = 0, bw = 0, wr0 = 0, wc0 = 0, frame = 0, blk = 0;
     const FrameDesc *fd = nullptr;
     int2 entry = make_int2(0, 0);
+    static_assert(!WC || (MODE == 0 && C::CL == 1), "cached W: pipeline levels, one CTA per window");
+    if constexpr (MODE == 2) {
+        if (entry_idx >= *A.count) return;  // planes beyond the session's count
+        entry = A.entries[A.wrep[entry_idx]];
+    }
     if constexpr (MODE == 0) {
         entry = entry_in.x >= 0 ? entry_in : A.entries[entry_idx];
+    }
+    constexpr bool cached = WC;
+    constexpr bool PIPE = MODE == 0 || MODE == 2;  // window from a frame (vs. the operator's arrays)
+    if constexpr (PIPE) {
         frame = entry.x;
         blk = entry.y;
         fd = A.frames + frame;
@@ -438,7 +460,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
 
     // ---- staging: classes -> weights (fse.py:105-119); x = w * select(w > 0, v, 0)
     double wsum = 0.0;
-    if constexpr (MODE == 0) {
+    if constexpr (PIPE) {
         // a warp stages window rows (lane = column: coalesced mask / image
         // reads, no index division); the global loads of RB rows are issued
         // before any of their math so their latencies overlap
@@ -496,7 +518,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
                         }
                         const double v = (double)val[r];
                         xs[i * N + j] = w > 0.0 ? (T)(w * v) : (T)0;
-                        ws[i * N + j] = (T)w;
+                        if constexpr (!cached) ws[i * N + j] = (T)w;
                         wsum += w;
                     }
                 }
@@ -528,7 +550,10 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     // Lanes take columns n (conflict-free sample reads), warps take k1 = warp +
     // NW r, so one read of x[m][n], w[m][n] feeds KR outputs; the twiddle
     // index is warp-uniform (broadcast read).
-    {
+    // (DOX / DOW: a cached window skips the w half, the cache's producer
+    // launch the x half)
+    auto column_pass = [&](auto dox_, auto dow_) {
+        constexpr bool DOX = decltype(dox_)::value, DOW = decltype(dow_)::value;
         constexpr int K1N = F / 4 + 1, KR = (K1N + NW - 1) / NW;
         for (int nc = 0; nc < N; nc += 32) {
             const int n = nc + lane;
@@ -541,19 +566,26 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
                     kk[r] = 0;
                 }
                 for (int m = 0; m < M; m += 2) {
-                    const T xv = xs[m * N + n], wv = ws[m * N + n];
                     const bool odd = m + 1 < M;
-                    const T xu = odd ? xs[(m + 1) * N + n] : (T)0, wu = odd ? ws[(m + 1) * N + n] : (T)0;
+                    T xv = (T)0, wv = (T)0, xu = (T)0, wu = (T)0;
+                    if constexpr (DOX) {
+                        xv = xs[m * N + n];
+                        xu = odd ? xs[(m + 1) * N + n] : (T)0;
+                    }
+                    if constexpr (DOW) {
+                        wv = ws[m * N + n];
+                        wu = odd ? ws[(m + 1) * N + n] : (T)0;
+                    }
 #pragma unroll
                     for (int r = 0; r < KR; ++r) {
                         const int k1 = warp + NW * r;
                         if (k1 < K1N) {
                             const T2 tv = tw[kk[r]];
-                            Xe[r] = cfma(T2{xv, -xv}, tv, Xe[r]);  // x e^{-j theta}
-                            We[r] = cfma(T2{wv, -wv}, tv, We[r]);
+                            if constexpr (DOX) Xe[r] = cfma(T2{xv, -xv}, tv, Xe[r]);  // x e^{-j theta}
+                            if constexpr (DOW) We[r] = cfma(T2{wv, -wv}, tv, We[r]);
                             const T2 tu = tw[(kk[r] + k1) & (F - 1)];
-                            Xo[r] = cfma(T2{xu, -xu}, tu, Xo[r]);
-                            Wo[r] = cfma(T2{wu, -wu}, tu, Wo[r]);
+                            if constexpr (DOX) Xo[r] = cfma(T2{xu, -xu}, tu, Xo[r]);
+                            if constexpr (DOW) Wo[r] = cfma(T2{wu, -wu}, tu, Wo[r]);
                             kk[r] = (kk[r] + 2 * k1) & (F - 1);
                         }
                     }
@@ -562,17 +594,29 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
                 for (int r = 0; r < KR; ++r) {
                     const int k1 = warp + NW * r;
                     if (k1 < K1N) {
-                        Yx[k1 * N + n] = cadd(Xe[r], Xo[r]);
-                        Yw[k1 * N + n] = cadd(We[r], Wo[r]);
+                        if constexpr (DOX) Yx[k1 * N + n] = cadd(Xe[r], Xo[r]);
+                        if constexpr (DOW) Yw[k1 * N + n] = cadd(We[r], Wo[r]);
                         if (k1 != F / 4) {
-                            const T2 dx = csub(Xe[r], Xo[r]), dw = csub(We[r], Wo[r]);
-                            Yx[(F / 2 - k1) * N + n] = T2{dx.x, -dx.y};
-                            Yw[(F / 2 - k1) * N + n] = T2{dw.x, -dw.y};
+                            if constexpr (DOX) {
+                                const T2 dx = csub(Xe[r], Xo[r]);
+                                Yx[(F / 2 - k1) * N + n] = T2{dx.x, -dx.y};
+                            }
+                            if constexpr (DOW) {
+                                const T2 dw = csub(We[r], Wo[r]);
+                                Yw[(F / 2 - k1) * N + n] = T2{dw.x, -dw.y};
+                            }
                         }
                     }
                 }
             }
         }
+    };
+    {
+        using Yes = std::true_type;
+        using No = std::false_type;
+        if constexpr (MODE == 2) column_pass(No{}, Yes{});
+        else if constexpr (cached) column_pass(Yes{}, No{});
+        else column_pass(Yes{}, Yes{});
     }
     __syncthreads();
     FSE_CLK(2);
@@ -675,22 +719,44 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     };
     T2 G[NB];
     unsigned valid = 0;  // bit j: bin j is a canonical in-range bin
-    partials(Yx);
-    __syncthreads();
+    if constexpr (MODE != 2) {
+        partials(Yx);
+        __syncthreads();
 #pragma unroll
-    for (int j = 0; j < NB; ++j) {
-        const int u = u0 + RSTEP * j;
-        G[j] = T2{0, 0};
-        if (u < R1 && !((u == 0 || u == F / 2) && v > F / 2)) {
-            G[j] = combine(u);
-            valid |= 1u << j;
+        for (int j = 0; j < NB; ++j) {
+            const int u = u0 + RSTEP * j;
+            G[j] = T2{0, 0};
+            if (u < R1 && !((u == 0 || u == F / 2) && v > F / 2)) {
+                G[j] = combine(u);
+                valid |= 1u << j;
+            }
         }
+        __syncthreads();
     }
-    __syncthreads();
     FSE_CLK(3);
-    partials_w(Yw);
-    __syncthreads();
+    if constexpr (!cached) {
+        partials_w(Yw);
+        __syncthreads();
+    }
     FSE_CLK(1000);
+    // a cached window's half rows come from the session's W cache (the bits
+    // the combine below would produce: the producer is this very code)
+    const T2 *wcache = nullptr;
+    if constexpr (cached) wcache = reinterpret_cast<const T2 *>(A.wplanes) + (size_t)wc * (R1 * F);
+    if constexpr (MODE == 2) {
+        // producer: the half rows go to the cache plane and the CTA is done
+        T2 *plane = reinterpret_cast<T2 *>(A.wplanes) + (size_t)entry_idx * (R1 * F);
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+            const int u = u0 + RSTEP * j;
+            if (u < R1) plane[u * F + v] = combine(u);
+        }
+        return;
+    }
+    auto whalf = [&](int u) -> T2 {
+        if constexpr (cached) return wcache[u * F + v];
+        else return combine(u);
+    };
     // W half rows 0..F/2; with EXT (one CTA per window) also the negative
     // rows W[-u][-v] = conj W[u][v] at once: they land in the dead x/w/Y
     // staging bytes below the half rows, while `part` (above them) is still
@@ -704,7 +770,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         for (int j = 0; j < NB; ++j) {
             const int u = u0 + RSTEP * j;
             T2 wv = T2{0, 0};
-            if (u < R1) wv = combine(u);
+            if (u < R1) wv = whalf(u);
             __syncthreads();
             if (u < R1) Wext[u * F + v] = wv;
         }
@@ -713,7 +779,7 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
         for (int j = 0; j < NB; ++j) {
             const int u = u0 + RSTEP * j;
             if (u < R1) {
-                const T2 wv = combine(u);
+                const T2 wv = whalf(u);
                 Wext[(u + (C::EXT ? F / 2 : 0)) * F + v] = wv;
                 if (MIRROR_NOW && u >= 1) Wext[(F / 2 - u) * F + ((F - v) & (F - 1))] = T2{wv.x, -wv.y};
             }
@@ -1259,6 +1325,9 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
     if constexpr (CL > 1) cooperative_groups::this_cluster().sync();
 }
 
+// (The two code paths as separate __noinline__ functions were tried: the
+// by-reference kernel parameters then live in local memory and the computing
+// path spills 220 B instead of 64 B.)
 template <class C, int MODE, bool GUARD>
 __global__ void __launch_bounds__(C::NT, C::MINB) fse_fast_kernel(const FastArgs A, const FastLayout L) {
     extern __shared__ __align__(128) unsigned char sm[];
@@ -1268,6 +1337,15 @@ __global__ void __launch_bounds__(C::NT, C::MINB) fse_fast_kernel(const FastArgs
     // launch gap between dependent levels overlaps this level's work
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if constexpr (MODE == 0 && !GUARD && C::CL == 1) {
+        // a window whose W is in the session's cache takes the twin code path
+        // without the weight half of the set-up (uniform over the CTA)
+        const int wc = A.wslot ? A.wslot[blockIdx.x] : -1;
+        if (wc >= 0) {
+            fast_window<C, MODE, GUARD, typename C::T, true>(A, L, blockIdx.x, sm, make_int2(-1, -1), wc);
+            return;
+        }
+    }
     fast_window<C, MODE, GUARD, typename C::T>(A, L, blockIdx.x, sm);
 }
 
@@ -1386,5 +1464,8 @@ int fast_dataflow(int dtype, int F, const FastArgs &a, int Mmax, int Nmax, int m
 int fast_redo(int F, const FastArgs &a, int max_entries, int Mmax, int Nmax, int model_n,
               cudaStream_t s);
 int fast_windows(int dtype, int F, const FastArgs &a, int grid, cudaStream_t s);
+// W-cache producer (MODE 2): plane p < *a.count from window a.entries[a.wrep[p]], grid = plane capacity
+int fast_wplanes(int dtype, int F, const FastArgs &a, int grid, int Mmax, int Nmax, int model_n,
+                 cudaStream_t s);
 
 }  // namespace fse

@@ -351,6 +351,21 @@ int fast_redo(int F, const FastArgs &a, int max_entries, int Mmax, int Nmax, int
     return launch_redo<Fast32<double>>(a, max_entries, Mmax, Nmax, model_n, s);
 }
 
+// One variant per (precision, F): every variant of one F forms W with the same
+// operation order (the column pass sums over m, the row pass over n, whatever
+// the warp count), so its planes serve all of them.
+int fast_wplanes(int dtype, int F, const FastArgs &a, int grid, int Mmax, int Nmax, int model_n,
+                 cudaStream_t s) {
+    if (dtype == FSE_F32) {
+        if (F == 128) return launch<Fast128<float>, 2, false>(a, grid, Mmax, Nmax, model_n, s);
+        if (F == 64) return launch<Fast64<float>, 2, false>(a, grid, Mmax, Nmax, model_n, s);
+        return launch<Fast32<float>, 2, false>(a, grid, Mmax, Nmax, model_n, s);
+    }
+    if (F == 128) return launch<Fast128D, 2, false>(a, grid, Mmax, Nmax, model_n, s);
+    if (F == 64) return launch<Fast64<double>, 2, false>(a, grid, Mmax, Nmax, model_n, s);
+    return launch<Fast32<double>, 2, false>(a, grid, Mmax, Nmax, model_n, s);
+}
+
 int fast_windows(int dtype, int F, const FastArgs &a, int grid, cudaStream_t s) {
     if (dtype == FSE_F32) {
         if (F == 128) return launch<Fast128<float>, 1, false>(a, grid, a.M, a.N, 0, s);
