@@ -566,16 +566,12 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
                     kk[r] = 0;
                 }
                 for (int m = 0; m < M; m += 2) {
-                    const bool odd = m + 1 < M;
                     T xv = (T)0, wv = (T)0, xu = (T)0, wu = (T)0;
-                    if constexpr (DOX) {
-                        xv = xs[m * N + n];
-                        xu = odd ? xs[(m + 1) * N + n] : (T)0;
-                    }
-                    if constexpr (DOW) {
-                        wv = ws[m * N + n];
-                        wu = odd ? ws[(m + 1) * N + n] : (T)0;
-                    }
+                    if constexpr (DOX) xv = xs[m * N + n];
+                    if constexpr (DOW) wv = ws[m * N + n];
+                    const bool odd = m + 1 < M;
+                    if constexpr (DOX) xu = odd ? xs[(m + 1) * N + n] : (T)0;
+                    if constexpr (DOW) wu = odd ? ws[(m + 1) * N + n] : (T)0;
 #pragma unroll
                     for (int r = 0; r < KR; ++r) {
                         const int k1 = warp + NW * r;
@@ -1328,7 +1324,12 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
 // (The two code paths as separate __noinline__ functions were tried: the
 // by-reference kernel parameters then live in local memory and the computing
 // path spills 220 B instead of 64 B.)
-template <class C, int MODE, bool GUARD>
+// TWIN: the kernel also holds the cached-W code path (launched for sessions
+// with a weight-spectrum cache).  Sessions without one launch the TWIN = false
+// instance, which is the kernel as it was before the cache existed: with the
+// twin inlined beside it ptxas schedules the computing path differently (its
+// x row pass 12.9 k -> 36.8 k cycles per window, +3% on config 4).
+template <class C, int MODE, bool GUARD, bool TWIN = false>
 __global__ void __launch_bounds__(C::NT, C::MINB) fse_fast_kernel(const FastArgs A, const FastLayout L) {
     extern __shared__ __align__(128) unsigned char sm[];
     // programmatic dependent launch (level launches, fse_inst_fast.cu): let the
@@ -1337,7 +1338,8 @@ __global__ void __launch_bounds__(C::NT, C::MINB) fse_fast_kernel(const FastArgs
     // launch gap between dependent levels overlaps this level's work
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    if constexpr (MODE == 0 && !GUARD && C::CL == 1) {
+    if constexpr (TWIN) {
+        static_assert(MODE == 0 && !GUARD && C::CL == 1, "cached W: plain pipeline levels");
         // a window whose W is in the session's cache takes the twin code path
         // without the weight half of the set-up (uniform over the CTA)
         const int wc = A.wslot ? A.wslot[blockIdx.x] : -1;

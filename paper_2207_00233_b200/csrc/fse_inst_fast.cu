@@ -216,14 +216,14 @@ static bool pdl_enabled() {
     return on;
 }
 
-template <class C, int MODE, bool GUARD>
-static int launch(const FastArgs &a, int grid, int Mmax, int Nmax, int model_n, cudaStream_t s) {
+template <class C, int MODE, bool GUARD, bool TWIN = false>
+static int launch_as(const FastArgs &a, int grid, int Mmax, int Nmax, int model_n, cudaStream_t s) {
     FastLayout L = fast_layout<typename C::T>(C::F, C::NWT, Mmax, Nmax, model_n, a.iterations, C::HALF ? 2 : (C::EXT ? 1 : 0));
 #ifdef FSE_SMEM_PAD
     L.total += FSE_SMEM_PAD;  // dev: occupancy sensitivity experiments
 #endif
-    auto kern = fse_fast_kernel<C, MODE, GUARD>;
-    if (int rc = ensure_smem<KTag<C, std::integral_constant<int, MODE>, std::integral_constant<bool, GUARD>>>((const void *)kern, L.total)) return rc;
+    auto kern = fse_fast_kernel<C, MODE, GUARD, TWIN>;
+    if (int rc = ensure_smem<KTag<C, std::integral_constant<int, MODE>, std::integral_constant<bool, GUARD>, std::integral_constant<bool, TWIN>>>((const void *)kern, L.total)) return rc;
     if (grid > 0) {
         if (pdl_enabled()) {
             cudaLaunchConfig_t cfg = {};
@@ -244,6 +244,16 @@ static int launch(const FastArgs &a, int grid, int Mmax, int Nmax, int model_n, 
         g_launches.fetch_add(1, std::memory_order_relaxed);
     }
     return FSE_OK;
+}
+
+// Level launches of a session with a weight-spectrum cache (a.wslot set) use
+// the instance that also holds the cached-W path.
+template <class C, int MODE, bool GUARD>
+static int launch(const FastArgs &a, int grid, int Mmax, int Nmax, int model_n, cudaStream_t s) {
+    if constexpr (MODE == 0 && !GUARD && C::CL == 1) {
+        if (a.wslot) return launch_as<C, MODE, GUARD, true>(a, grid, Mmax, Nmax, model_n, s);
+    }
+    return launch_as<C, MODE, GUARD, false>(a, grid, Mmax, Nmax, model_n, s);
 }
 
 template <class C>
