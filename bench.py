@@ -441,7 +441,7 @@ def run_b200(a, rank, world, local_rank):
     fp32_peak = max(peaks["ffma"], peaks["ffma2"])
 
     traffic = None
-    tpath = os.path.join(REPO, "profiles", "traffic_r2.json")
+    tpath = os.path.join(REPO, "profiles", "traffic_r4.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath))
 

@@ -17,7 +17,7 @@ tag = {"float": "If", "double": "Id"}[ty] + "Li" + F
 work = "FFMA2" if ty == "float" else "DFMA"
 for f in re.split(r"\n\s+Function : ", sass)[1:]:
     name = f.split("\n")[0]
-    if "15fse_fast_kernel" not in name or tag not in name or "EEELi0ELb0EEEv" not in name:
+    if "15fse_fast_kernel" not in name or tag not in name or not re.search(r"EEELi0ELb0E(Lb[01]E)?EEv", name):
         continue
     ins = []
     for line in f.split("\n"):
