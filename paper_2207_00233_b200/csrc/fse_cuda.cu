@@ -65,8 +65,9 @@ static std::atomic<int> g_groups{[] {
 // to FSE_WCACHE_PLANES planes (default 65536) and FSE_WCACHE_MB of them (default
 // 4096), and the level kernels load it
 // from L2 instead of running the w half of the set-up.  On for sessions of at
-// least FSE_WCACHE_ENTRIES windows (default 2048: below that the three
-// classification launches cost more than they save).  FSE_WCACHE=0 or
+// least FSE_WCACHE_ENTRIES windows (default 2048) and FSE_WCACHE_WIDTH windows
+// per level on average (default 1024): below that the classification and
+// producer launches cost more than they save.  FSE_WCACHE=0 or
 // fse_set_wcache(0) turns it off; results are bit-identical either way.
 static std::atomic<int> g_wcache{[] {
     const char *e = getenv("FSE_WCACHE");
@@ -676,7 +677,12 @@ static int session_open(int32_t n, FsePlan *const *plans, void *const *images, c
     // share of a window for the classification to pay (measured 180 vs 172 ms)
     if (fast_session && !guard_session && g_wcache.load() > 0 && !dataflow_enabled() &&
         F1 >= env_int("FSE_WCACHE_MIN_F", 64) &&
-        n_entries >= (size_t)std::max(1, env_int("FSE_WCACHE_ENTRIES", 2048)) && n_entries < ((size_t)1 << 30)) {
+        n_entries >= (size_t)std::max(1, env_int("FSE_WCACHE_ENTRIES", 2048)) && n_entries < ((size_t)1 << 30) &&
+        // throughput-bound sessions only: with levels narrower than a few waves
+        // the set-up is not what a level waits for, and the classification and
+        // producer launches cost more than the cached set-ups save (configs 2
+        // and 3: 8.13 vs 7.81 ms and 36.1 vs 35.0 ms with the cache on / off)
+        n_entries >= (size_t)std::max(0, env_int("FSE_WCACHE_WIDTH", 1024)) * (size_t)std::max(n_levels, 1)) {
         const size_t elem = 2 * (dtype == FSE_F64 ? sizeof(double) : sizeof(float));
         const size_t plane_bytes = (size_t)(F1 / 2 + 1) * F1 * elem;
         wa.min_count = std::max(1, env_int("FSE_WCACHE_MIN", 2));

@@ -53,7 +53,7 @@ def _stats(fn):
     return out, w.value, h.value, p.value
 
 
-FORCE = dict(FSE_WCACHE_ENTRIES=1, FSE_WCACHE_MIN_F=32)
+FORCE = dict(FSE_WCACHE_ENTRIES=1, FSE_WCACHE_MIN_F=32, FSE_WCACHE_WIDTH=0)
 
 
 @pytest.mark.parametrize("prec,B,F,crop", [
@@ -110,7 +110,8 @@ def test_cached_path_matches_reference_golden(golden, i):
 
 def test_cache_in_batches_and_default_threshold():
     """conceal_batch over several frames shares planes across frames; small
-    sessions (below FSE_WCACHE_ENTRIES windows) leave the cache off."""
+    sessions (below FSE_WCACHE_ENTRIES windows, or FSE_WCACHE_WIDTH windows per
+    level) leave the cache off."""
     sc = [synth.config_scene(4, f) for f in range(3)]
     imgs = np.stack([s[0][:160, :224] for s in sc])
     msks = np.stack([s[1][:160, :224] for s in sc])

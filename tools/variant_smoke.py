@@ -17,6 +17,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 # the cache classifies every session, however small, in this process
 os.environ.setdefault("FSE_WCACHE_ENTRIES", "1")
 os.environ.setdefault("FSE_WCACHE_MIN_F", "32")
+os.environ.setdefault("FSE_WCACHE_WIDTH", "0")
 
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
