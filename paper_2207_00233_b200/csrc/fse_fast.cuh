@@ -1232,7 +1232,21 @@ __device__ __forceinline__ void fast_window(const FastArgs &A, const FastLayout 
                         wl[q] = lo[j * RSTEP * F];
                         wh[q] = hi[j * RSTEP * F];
                     } else {
-                        wl[q] = (j < jl ? loW : lo)[j * RSTEP * F];
+                        // plain plane, narrow-level variant: row (x0 + RSTEP j) mod F by
+                        // masking the byte offset (an add and an AND per bin instead of the
+                        // compare and two-base select).  Only there: config 2 7.81 -> 7.73 ms,
+                        // but the 6-warp throughput kernel loses 8% with it (559 vs 519 ms on
+                        // config 4: the two dependent ALU operations sit in front of every
+                        // u-a gather), profiles/r4/ab_loop/
+                        if constexpr (C::LGC > 0 && !IS_F32) {
+                            static_assert(((F * F * sizeof(T2)) & (F * F * sizeof(T2) - 1)) == 0, "power-of-two plane");
+                            const unsigned ob = (unsigned)((x0 * F + cm) * (int)sizeof(T2));
+                            wl[q] = *reinterpret_cast<const T2 *>(reinterpret_cast<const char *>(Wext) +
+                                                                  ((ob + (unsigned)(j * RSTEP * F * sizeof(T2))) &
+                                                                   (unsigned)(F * F * sizeof(T2) - 1)));
+                        } else {
+                            wl[q] = (j < jl ? loW : lo)[j * RSTEP * F];
+                        }
                         wh[q] = hi[j * RSTEP * F];
                     }
                 }
