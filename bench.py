@@ -139,32 +139,48 @@ class ClockSampler:
         except Exception:
             pass
         self.rows = []
-        self._stop = threading.Event()
+        self._p = None
         self._t = None
 
     def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                row = [x.strip() for x in out.split(",")] if out else []
-                if len(row) == 6:
-                    self.rows.append(row)
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        # ONE nvidia-smi process in loop mode (-lms 200), started before the timed
+        # region and killed after it, as the profiling recipe does: a process per
+        # sample costs ~0.3 s of host CPU and a driver lock each, which showed up as
+        # host stalls inside the timed steps (step 588-779 ms against 519 ms of kernels)
+        for line in self._p.stdout:
+            row = [x.strip() for x in line.strip().split(",")]
+            if len(row) == 6:
+                self.rows.append(row)
+                self._first.set()
 
     def __enter__(self):
+        self._first = threading.Event()
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                        "--format=csv,noheader,nounits", "-lms", "200"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self._p = None
+            return self
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        self._first.wait(3.0)  # the process is up and sampling before the timed region starts
+        self._start = len(self.rows)  # samples taken before the region are not "under load"
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join()
+        if self._p is None:
+            return
+        self._p.terminate()
+        try:
+            self._p.wait(timeout=3)
+        except Exception:
+            self._p.kill()
+        self._t.join(timeout=3)
 
     def summary(self):
+        # a region shorter than the sampling period keeps the sample taken just before it
+        self.rows = self.rows[getattr(self, "_start", 0):] or self.rows[-1:]
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
@@ -423,7 +439,8 @@ def run_b200(a, rank, world, local_rank):
                   "hit_share": (wch.value / wcw.value) if wcw.value else 0.0}
         return {"ms": ms, "kernel_ms": kms.value / a.steps, "launches": launches, "wcache": wcache,
                 "level_launches": int(wl.value),
-                "plan_ms": float(np.mean(plan_ms)) if plan_ms else None, "redo": redo / a.steps,
+                "plan_ms": float(np.mean(plan_ms)) if plan_ms else None,
+                "plan_ms_steps": [round(x, 1) for x in plan_ms], "redo": redo / a.steps,
                 "clocks": clk.summary() if clk else None}
 
     head = measure(a.precision, True)
@@ -527,7 +544,7 @@ def run_b200(a, rank, world, local_rank):
             "lost_mpixel_per_s": lost_px_all * a.steps / (head["ms"] * 1e-3) / 1e6,
             "blocks_per_step": blocks_all, "lost_pixels_per_step": lost_px_all,
             "levels_per_step": levels,
-            "host_enqueue_ms_per_step": head["plan_ms"],
+            "host_enqueue_ms_per_step": head["plan_ms"], "host_enqueue_ms_steps": head["plan_ms_steps"],
             "kernel_ms_per_step": head["kernel_ms"],
             "fp32_guard_fp64_redo_per_step": head["redo"],
             "weight_spectrum_cache": head["wcache"],
