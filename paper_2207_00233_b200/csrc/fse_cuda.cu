@@ -90,6 +90,7 @@ struct PinnedStage {
     size_t cap = 0;
     cudaEvent_t ev = nullptr;
     bool busy = false;  // acquired, its copy not queued yet
+    int dev = 0;        // the device its event belongs to: a buffer serves that device's sessions only
 };
 static std::mutex g_stage_mu;
 static std::vector<PinnedStage> g_stage;
@@ -145,15 +146,20 @@ static int stage_acquire(size_t bytes, int *slot, unsigned char **ptr) {
     // the smallest idle buffer that fits; otherwise a new one.  Buffers are
     // never freed here: cudaFreeHost would synchronise the device and drain
     // the level pipeline.  Past 16 buffers, wait for the oldest fitting one.
+    int dev = 0;
+    cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(g_stage_mu);
     auto idle = [](const PinnedStage &b) { return !b.busy && (!b.ev || cudaEventQuery(b.ev) == cudaSuccess); };
-    int pick = -1;
-    for (int i = 0; i < (int)g_stage.size(); ++i)
+    int pick = -1, mine = 0;
+    for (int i = 0; i < (int)g_stage.size(); ++i) {
+        if (g_stage[i].dev != dev) continue;
+        ++mine;
         if (g_stage[i].cap >= bytes && idle(g_stage[i]) && (pick < 0 || g_stage[i].cap < g_stage[pick].cap))
             pick = i;
-    if (pick < 0 && g_stage.size() >= 16) {
+    }
+    if (pick < 0 && mine >= 16) {
         for (int i = 0; i < (int)g_stage.size(); ++i)
-            if (g_stage[i].cap >= bytes && !g_stage[i].busy) {
+            if (g_stage[i].dev == dev && g_stage[i].cap >= bytes && !g_stage[i].busy) {
                 cudaEventSynchronize(g_stage[i].ev);
                 pick = i;
                 break;
@@ -161,6 +167,7 @@ static int stage_acquire(size_t bytes, int *slot, unsigned char **ptr) {
     }
     if (pick < 0) {
         PinnedStage b;
+        b.dev = dev;
         b.cap = std::max(bytes, (size_t)1 << 20) * 5 / 4;
         if (cudaMallocHost(&b.p, b.cap) != cudaSuccess) return fail(FSE_ENOMEM, "pinned staging alloc");
         if (cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming) != cudaSuccess) {
