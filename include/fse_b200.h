@@ -179,9 +179,10 @@ int fse_set_groups(int32_t n);
  * _kernel.pyx:148 depends only on a window's shape and class map
  * (fse.py:105-119), so windows of one call that share both share W.  1
  * (default; FSE_WCACHE=0 sets the default off): before the first level every
- * window's class map is hashed and compared on the device (sessions of
- * >= 2,048 windows and >= 1,024 windows per level on average, F >= 64: only
- * throughput-bound sessions gain), each W shared by
+ * window's class map is hashed and compared on the device (F >= 64; sessions
+ * of >= 2,048 windows and >= 1,024 windows per level on average: a plane per
+ * map shared by >= 2 windows; sessions of narrower levels and >= 1,024 windows:
+ * a plane for every window, if the plane capacity covers them), each W shared by
  * >= 2 windows is computed once, and the level kernels load it instead of
  * running the weight half of their set-up.  Results are bit-identical to 0
  * (every window computes its own W).  Process-wide. */

@@ -64,10 +64,9 @@ static std::atomic<int> g_groups{[] {
 // (FSE_WCACHE_MIN=1: every W) is computed once before the first level, up
 // to FSE_WCACHE_PLANES planes (default 65536) and FSE_WCACHE_MB of them (default
 // 4096), and the level kernels load it
-// from L2 instead of running the w half of the set-up.  On for sessions of at
-// least FSE_WCACHE_ENTRIES windows (default 2048) and FSE_WCACHE_WIDTH windows
-// per level on average (default 1024): below that the classification and
-// producer launches cost more than they save.  FSE_WCACHE=0 or
+// from L2 instead of running the w half of the set-up.  Which sessions use it,
+// and with a plane for shared maps only or for every window: see session_open.
+// FSE_WCACHE=0 or
 // fse_set_wcache(0) turns it off; results are bit-identical either way.
 static std::atomic<int> g_wcache{[] {
     const char *e = getenv("FSE_WCACHE");
@@ -693,24 +692,31 @@ static int session_open(int32_t n, FsePlan *const *plans, void *const *images, c
     WCacheArgs wa{};
     size_t off_wkeys = 0, off_wrepslot = 0, off_wzero_end = 0, off_wff_end = 0, off_planes = 0;
     // F >= 64 by default: at F = 32 (config 5, B = 2) the set-up is too small a
-    // share of a window for the classification to pay (measured 180 vs 172 ms)
+    // share of a window for the classification to pay (measured 180 vs 172 ms).
+    // Two regimes (same-box A/Bs in profiles/r4/ab_gate):
+    //  * throughput-bound sessions (>= FSE_WCACHE_WIDTH windows per level on
+    //    average, default 1024, and >= FSE_WCACHE_ENTRIES windows, default 2048):
+    //    a plane for every map shared by >= 2 windows (config 4: 534 -> 523 ms);
+    //  * sessions of narrow levels, where a window's latency sets the time: a
+    //    plane for EVERY window, so that no window runs the slower computing
+    //    path of the twin kernel, and only when the plane capacity covers them
+    //    all (config 2 fp64 7.75 -> 7.37 ms, configs 1 / 3 / 5 B=4 unchanged;
+    //    with shared maps only, the misses made it a loss: 7.88 ms).
+    const size_t wc_elem = 2 * (dtype == FSE_F64 ? sizeof(double) : sizeof(float));
+    const size_t wc_plane_bytes = (size_t)(F1 / 2 + 1) * std::max(F1, 1) * wc_elem;
+    const size_t wc_max_planes = std::max<size_t>(1, std::min<size_t>(
+        (size_t)std::max(1, env_int("FSE_WCACHE_PLANES", 65536)),
+        // at most FSE_WCACHE_MB of planes (default 4 GiB: 127 k planes at fp64 F = 64, 31 k at F = 128)
+        ((size_t)std::max(1, env_int("FSE_WCACHE_MB", 4096)) << 20) / wc_plane_bytes));
+    const bool wc_wide = n_entries >= (size_t)std::max(0, env_int("FSE_WCACHE_WIDTH", 1024)) * (size_t)std::max(n_levels, 1) &&
+                         n_entries >= (size_t)std::max(1, env_int("FSE_WCACHE_ENTRIES", 2048));
+    const bool wc_all = !wc_wide && n_entries >= (size_t)std::max(1, env_int("FSE_WCACHE_ENTRIES_ALL", 1024)) &&
+                        n_entries <= wc_max_planes;
     if (fast_session && !guard_session && g_wcache.load() > 0 && !dataflow_enabled() &&
-        F1 >= env_int("FSE_WCACHE_MIN_F", 64) &&
-        n_entries >= (size_t)std::max(1, env_int("FSE_WCACHE_ENTRIES", 2048)) && n_entries < ((size_t)1 << 30) &&
-        // throughput-bound sessions only: with levels narrower than a few waves
-        // the set-up is not what a level waits for, and the classification and
-        // producer launches cost more than the cached set-ups save (configs 2
-        // and 3: 8.13 vs 7.81 ms and 36.1 vs 35.0 ms with the cache on / off)
-        n_entries >= (size_t)std::max(0, env_int("FSE_WCACHE_WIDTH", 1024)) * (size_t)std::max(n_levels, 1)) {
-        const size_t elem = 2 * (dtype == FSE_F64 ? sizeof(double) : sizeof(float));
-        const size_t plane_bytes = (size_t)(F1 / 2 + 1) * F1 * elem;
-        wa.min_count = std::max(1, env_int("FSE_WCACHE_MIN", 2));
-        // (a plane serves >= 2 windows, so n / 2 planes are enough)
-        S->wc_cap = (int)std::min<size_t>(std::max<size_t>(wa.min_count > 1 ? n_entries / 2 : n_entries, 1),
-                                          (size_t)std::max(1, env_int("FSE_WCACHE_PLANES", 65536)));
-        // and at most FSE_WCACHE_MB of planes (default 4 GiB: 127 k planes at fp64 F = 64, 31 k at F = 128)
-        S->wc_cap = (int)std::max<size_t>(1, std::min<size_t>((size_t)S->wc_cap,
-                                                              ((size_t)std::max(1, env_int("FSE_WCACHE_MB", 4096)) << 20) / plane_bytes));
+        F1 >= env_int("FSE_WCACHE_MIN_F", 64) && (wc_wide || wc_all) && n_entries < ((size_t)1 << 30)) {
+        wa.min_count = std::max(1, env_int("FSE_WCACHE_MIN", wc_wide ? 2 : 1));
+        // (a plane shared by >= 2 windows: n / 2 planes are enough)
+        S->wc_cap = (int)std::min<size_t>(std::max<size_t>(wa.min_count > 1 ? n_entries / 2 : n_entries, 1), wc_max_planes);
         size_t slots = 1024;
         while (slots < 2 * n_entries) slots <<= 1;
         wa.tmask = (uint32_t)(slots - 1);
@@ -729,7 +735,7 @@ static int session_open(int32_t n, FsePlan *const *plans, void *const *images, c
         const size_t off_wrep = S->off_wslot + up256(sizeof(int32_t) * n_entries);
         const size_t off_sig = off_wrep + up256(sizeof(int32_t) * (size_t)S->wc_cap);
         off_planes = off_sig + up256(sizeof(unsigned long long) * n_entries * (size_t)wa.SW);
-        bytes = off_planes + plane_bytes * (size_t)S->wc_cap;
+        bytes = off_planes + wc_plane_bytes * (size_t)S->wc_cap;
         // offsets into pointers once the buffer exists (below)
         wa.counters = reinterpret_cast<int *>(S->off_wcnt);
         wa.keys = reinterpret_cast<unsigned long long *>(off_wkeys);
