@@ -576,6 +576,7 @@ def run_small_bench(a, rank, world, local_rank):
 
     import paper_2207_00233_b200 as P
     from paper_2207_00233_b200 import _lib, synth
+    from paper_2207_00233_b200.conceal import balance_for_device
 
     torch.cuda.set_device(local_rank % max(1, torch.cuda.device_count()))
     params = P.FseParams(d=D, rho=RHO, delta=DELTA, gamma=GAMMA, iterations=100, block_size=B, fft_size=F)
@@ -593,6 +594,7 @@ def run_small_bench(a, rank, world, local_rank):
         def step():
             work.copy_(src)
             plan = P.build_plan(mask, params, order)
+            balance_for_device(plan, params, precision)
             P.run_frames_device([plan], [work], [msk], [out], params, precision)
             return plan
 
@@ -649,6 +651,7 @@ def run_strips_bench(a, rank, world, local_rank):
 
     import paper_2207_00233_b200 as P
     from paper_2207_00233_b200 import _lib, strips, synth
+    from paper_2207_00233_b200.conceal import balance_for_device
 
     torch.cuda.set_device(local_rank % max(1, torch.cuda.device_count()))
     Bk = a.block
@@ -675,9 +678,10 @@ def run_strips_bench(a, rank, world, local_rank):
         work.copy_(src)
         t0 = time.perf_counter()
         if hg is not None:  # plan once, broadcast the bytes over a host (gloo) group
-            plan = strips.broadcast_plan(mask, params, "optimized", rank, dist, hg, 0)
+            plan = strips.broadcast_plan(mask, params, "optimized", rank, dist, hg, 0, precision=a.precision)
         else:
             plan = P.build_plan(mask, params)
+            balance_for_device(plan, params, a.precision)
         processed = (plan.ranks() != np.iinfo(np.int32).max).reshape(plan.rows, plan.cols)
         bands = strips.band_partition(processed.sum(axis=1), world, R)
         stats["plan_ms"] = 1e3 * (time.perf_counter() - t0)

@@ -117,6 +117,18 @@ int fse_plan_sizes(const FsePlan *plan, int32_t *sizes);
 int fse_plan_batches(const FsePlan *plan, int32_t *ptr, int32_t *blocks);
 /* dependency levels, CSR over processed blocks, ptr[n_levels+1] */
 int fse_plan_levels(const FsePlan *plan, int32_t *ptr, int32_t *blocks);
+/* Level balancing of a built plan (no reference counterpart: the reference's
+ * batches, conceal.py:148-163, stay as they are; this only changes in which
+ * LAUNCH a block runs).  Every block sits at its earliest dependency level;
+ * blocks with slack (no dependent needs them yet) move from levels wider than
+ * `narrow` windows into later levels that still have free slots: up to `narrow`
+ * windows in levels that stay at most that wide (the caller passes the SM
+ * count: those levels run one window per SM), and, if wave > 0, up to the next
+ * multiple of `wave` in wider levels (the resident windows of one wave).
+ * Ranks, batches and results are unchanged (only true dependences order the
+ * launches).  narrow = 0 leaves the plan as it is.  *moved (optional) = blocks
+ * that changed level. */
+int fse_plan_rebalance(FsePlan *plan, int32_t narrow, int32_t wave, int32_t *moved);
 /* effective rank per block (INT32_MAX = not processed) [rows*cols] */
 int fse_plan_ranks(const FsePlan *plan, int32_t *rank);
 /* ConcealReport.unconcealed_blocks, row-major */

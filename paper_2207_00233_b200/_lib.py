@@ -20,6 +20,7 @@ FSE_IPC_HANDLE_BYTES = 72
 EXPORTS = (
     "fse_last_error", "fse_version", "fse_run_windows", "fse_plan_build", "fse_plan_build_threads", "fse_plan_build_many",
     "fse_plan_free", "fse_plan_sizes", "fse_plan_batches", "fse_plan_levels", "fse_plan_ranks",
+    "fse_plan_rebalance",
     "fse_plan_unconcealed", "fse_plan_export_size", "fse_plan_export", "fse_plan_import", "fse_init_counts", "fse_schedule_all", "fse_conceal_frames",
     "fse_launch_count", "fse_timing_enable", "fse_timing_read", "fse_fma_probe",
     "fse_set_guard", "fse_guard_redo_count", "fse_set_dataflow", "fse_set_groups", "fse_set_track_below",
@@ -86,6 +87,7 @@ def lib():
             getattr(L, name).argtypes = [_vp, _pi32, _pi32]
         for name in ("fse_plan_sizes", "fse_plan_ranks", "fse_plan_unconcealed"):
             getattr(L, name).argtypes = [_vp, _pi32]
+        L.fse_plan_rebalance.argtypes = [_vp, _i32, _i32, _pi32]
         L.fse_plan_export_size.argtypes = [_vp]
         L.fse_plan_export_size.restype = ctypes.c_int64
         L.fse_plan_export.argtypes = [_vp, _vp, ctypes.c_int64]

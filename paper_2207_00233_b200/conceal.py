@@ -79,6 +79,14 @@ class Plan:
     def levels(self) -> list:
         return self._csr(_lib.lib().fse_plan_levels, self.n_levels, self.n_processed)
 
+    def rebalance(self, narrow: int, wave: int = 0) -> int:
+        """Level balancing (fse_plan_rebalance): blocks with slack move from levels
+        wider than ``narrow`` windows into later levels with free slots.  Ranks,
+        batches and results are unchanged.  Returns the number of moved blocks."""
+        moved = np.zeros(1, dtype=np.int32)
+        _lib.check(_lib.lib().fse_plan_rebalance(self.handle, int(narrow), int(wave), _lib.ptr32(moved)))
+        return int(moved[0])
+
     def ranks(self) -> np.ndarray:
         r = np.zeros(self.rows * self.cols, dtype=np.int32)
         _lib.check(_lib.lib().fse_plan_ranks(self.handle, _lib.ptr32(r)))
@@ -106,6 +114,39 @@ class Plan:
         u = np.zeros(max(self.n_unconcealed, 1), dtype=np.int32)
         _lib.check(_lib.lib().fse_plan_unconcealed(self.handle, _lib.ptr32(u)))
         return u[: self.n_unconcealed].tolist()
+
+
+_SM_COUNT: dict = {}
+
+
+def balance_for_device(plan: "Plan", params: FseParams, precision: str, frames: int = 1) -> int:
+    """Level balancing of a one-frame plan for the current CUDA device: narrow =
+    the SM count (levels of at most that many windows run one window per SM, at
+    a lone window's latency however few they are, so their free slots take
+    blocks of the wide levels for nothing).  Plans of a multi-frame call are
+    left alone: their levels merge across frames.  FSE_BALANCE=0 turns it off;
+    FSE_BALANCE_WAVE=1 selects the variant that only moves the last, partial
+    wave of a wide level (wave = SMs x resident CTAs per SM of the fast kernel),
+    also into levels of less than one wave."""
+    if frames != 1 or os.environ.get("FSE_BALANCE", "1") == "0":
+        return 0
+    # the pass is sequential (1.3 ms on a 1080p frame at B = 4, 9 ms on a 4K one, 65 ms on a 4K frame at
+    # B = 2, whose band-parallel plan itself takes 25 ms): skipped on the largest grids
+    if plan.rows * plan.cols > int(os.environ.get("FSE_BALANCE_MAX_BLOCKS", "600000")):
+        return 0
+    import torch
+
+    if not torch.cuda.is_available():
+        return 0
+    dev = torch.cuda.current_device()
+    sms = _SM_COUNT.get(dev)
+    if sms is None:
+        sms = _SM_COUNT[dev] = torch.cuda.get_device_properties(dev).multi_processor_count
+    F = params.fft_size if isinstance(params.fft_size, int) else 0
+    per_sm = {("fp64", 64): 3, ("fp32", 64): 4, ("fp64", 32): 6, ("fp32", 32): 8,
+              ("fp64", 128): 1, ("fp32", 128): 1}.get((precision, F), 0)
+    wave = sms * per_sm if os.environ.get("FSE_BALANCE_WAVE", "0") == "1" else 0
+    return plan.rebalance(sms, wave)
 
 
 def _order_code(order: str) -> int:
@@ -240,6 +281,8 @@ def plan_and_run(masks_host, images_dev, masks_dev, masks_out_dev, params: FsePa
         return []
     k0 = n if n < 4 else (first_chunk or max(1, -(-n // 8)))
     plans = build_plans(masks_host[:k0], params, order, plan_threads)
+    if n == 1:  # one frame: its levels are the launches, balance them (multi-frame levels merge across frames)
+        balance_for_device(plans[0], params, precision)
     run_frames_device(plans, images_dev[:k0], masks_dev[:k0],
                       None if masks_out_dev is None else masks_out_dev[:k0], params, precision)
     if k0 < n:
@@ -268,6 +311,7 @@ def conceal(image, mask, params: FseParams | None = None, order: str = OPTIMIZED
     msk = np.array(mask, dtype=np.uint8, copy=True)
     t0 = time.perf_counter()
     plan = build_plan(msk, params, order)
+    balance_for_device(plan, params, precision)
     tdt = torch.float64 if precision == "fp64" else torch.float32
     img_d = torch.from_numpy(img).to(device="cuda", dtype=tdt)
     msk_d = torch.from_numpy(msk).cuda()
@@ -438,6 +482,8 @@ def conceal_batch(images, masks, params: FseParams | None = None, order: str = O
     for c in range(len(bounds) - 1):
         lo, hi = bounds[c], bounds[c + 1]
         pl = build_plans(list(mh[lo:hi]), params, order, plan_threads)
+        if n == 1:
+            balance_for_device(pl[0], params, precision)
         mark(f"plan{c}")
         if c == 1:
             main.wait_event(up)

@@ -17,6 +17,7 @@
 // reference batches may share a launch as long as every lower-rank block whose
 // samples their window covers has finished: those dependencies define levels.
 #include <algorithm>
+#include <functional>
 #include <atomic>
 #include <climits>
 #include <limits>
@@ -960,6 +961,96 @@ void level_csr(Plan &P, const std::vector<int32_t> &level, int n_levels) {
         if (level[b] >= 0) P.level_blocks[fill[level[b]]++] = b;
 }
 
+// Level balancing (a pure re-leveling: ranks, batches and results unchanged).
+// level_pass puts every block at its EARLIEST level, which leaves a frame with a
+// few very wide first levels and a long tail of levels of a handful of windows
+// (1080p, 30% isolated losses: 3,356 ... 1 windows over 101 levels), each tail
+// level costing a lone window's latency with the GPU nearly empty.  A block may
+// run at any level between its earliest one and one below its earliest
+// DEPENDENT (a higher-rank block whose window covers it); blocks of a level
+// never read each other with nonzero weight whatever their ranks (a lower-rank
+// block sees a higher-rank one as lost), so only these true dependences order
+// the launches.  Walking the batches from last to first (every dependent of a
+// block lies in a later batch and is placed before it), a block of the last,
+// partial wave of a level wider than one wave moves to the latest level within
+// its slack that still has free slots: slots up to `narrow` in levels that stay
+// on the one-window-per-SM kernel, up to `wave` in levels of at most one wave.
+// The slack bound uses the same separable (2R+1)^2 minimum as level_pass's
+// maximum.
+int rebalance_levels(Plan &P, int narrow, int wave) {
+    const int n_levels = (int)P.level_ptr.size() - 1;
+    const int rows = P.rows, cols = P.cols;
+    if (n_levels < 3 || narrow < 1 || rows < 1 || cols < 1) return 0;
+    const int R = (P.d + P.B - 1) / P.B;
+    const int nb = rows * cols;
+    std::vector<int32_t> level(nb, -1);
+    // cap: how many windows a level may hold after accepting blocks; shed: how
+    // many it may give away.  A level wider than one wave gives away only its
+    // last, partial wave (and accepts nothing); a level of at most one wave
+    // accepts up to the wave (or up to `narrow` while it stays that narrow) and
+    // gives nothing away.  Without a wave size (wave = 0) every level wider
+    // than `narrow` may give away any block and only narrow levels accept.
+    std::vector<int32_t> load(n_levels, 0), cap(n_levels, 0), shed(n_levels, 0);
+    for (int l = 0; l < n_levels; ++l) {
+        load[l] = P.level_ptr[l + 1] - P.level_ptr[l];
+        for (int i = P.level_ptr[l]; i < P.level_ptr[l + 1]; ++i) level[P.level_blocks[i]] = l;
+        if (load[l] <= narrow) cap[l] = narrow;
+        else if (wave > 0 && load[l] <= wave) cap[l] = wave;
+        else cap[l] = load[l];
+        if (wave > 0) shed[l] = load[l] > wave ? load[l] % wave : 0;
+        else shed[l] = load[l] > narrow ? load[l] : 0;
+    }
+    // latest level <= l with a free slot (union-find over full levels; -1 = none)
+    std::vector<int32_t> nf(n_levels + 1);
+    for (int l = 0; l <= n_levels; ++l) nf[l] = l;  // index l + 1 stands for level l, index 0 = none
+    auto full = [&](int l) { return load[l] >= cap[l]; };
+    std::function<int(int)> find = [&](int i) {
+        while (nf[i] != i) {
+            nf[i] = nf[nf[i]];
+            i = nf[i];
+        }
+        return i;
+    };
+    for (int l = 0; l < n_levels; ++l)
+        if (full(l)) nf[l + 1] = l;  // points to the previous index
+    const int32_t kNone = INT32_MAX;
+    std::vector<int32_t> HM((size_t)rows * cols, kNone);  // min new level of later-batch blocks over row r, columns c +- R
+    const int n_batches = (int)P.batch_ptr.size() - 1;
+    int moved = 0;
+    for (int k = n_batches - 1; k >= 0; --k) {
+        const int i0 = P.batch_ptr[k], i1 = P.batch_ptr[k + 1];
+        for (int i = i0; i < i1; ++i) {
+            const int b = P.batch_blocks[i];
+            const int lb = level[b];
+            if (lb < 0 || shed[lb] <= 0) continue;  // its level gives nothing (more) away
+            const int r = b / cols, c = b - r * cols;
+            int32_t m = kNone;
+            for (int rr = std::max(0, r - R); rr <= std::min(rows - 1, r + R); ++rr)
+                m = std::min(m, HM[(size_t)rr * cols + c]);
+            const int ub = (m == kNone ? n_levels : m) - 1;  // latest level b may run at
+            if (ub <= lb) continue;
+            const int t = find(ub + 1) - 1;  // latest level <= ub with a free slot
+            if (t <= lb) continue;
+            --load[lb];
+            --shed[lb];
+            ++load[t];
+            if (full(t)) nf[t + 1] = t;
+            level[b] = t;
+            ++moved;
+        }
+        for (int i = i0; i < i1; ++i) {
+            const int b = P.batch_blocks[i];
+            if (level[b] < 0) continue;
+            const int r = b / cols, c = b - r * cols;
+            int32_t *row = &HM[(size_t)r * cols];
+            const int32_t lv = level[b];
+            for (int cc = std::max(0, c - R); cc <= std::min(cols - 1, c + R); ++cc) row[cc] = std::min(row[cc], lv);
+        }
+    }
+    if (moved) level_csr(P, level, n_levels);
+    return moved;
+}
+
 // Retry sweeps (conceal.py:69-94): sequential, row-major, each sees the
 // previous results; every retried block is its own batch.  Levels of retried
 // blocks continue the level rows HL.
@@ -1413,6 +1504,14 @@ int fse_plan_levels(const FsePlan *plan, int32_t *ptr, int32_t *blocks) {
     const fse::Plan &P = plan->p;
     std::copy(P.level_ptr.begin(), P.level_ptr.end(), ptr);
     std::copy(P.level_blocks.begin(), P.level_blocks.end(), blocks);
+    return FSE_OK;
+}
+
+int fse_plan_rebalance(FsePlan *plan, int32_t narrow, int32_t wave, int32_t *moved) {
+    if (!plan) return fail(FSE_EINVAL, "NULL plan");
+    if (narrow < 0 || wave < 0) return fail(FSE_EINVAL, "narrow and wave must be >= 0");
+    const int n = narrow > 0 ? fse::rebalance_levels(plan->p, narrow, wave) : 0;
+    if (moved) *moved = n;
     return FSE_OK;
 }
 

@@ -27,7 +27,7 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from .conceal import DeviceContext, Plan, build_plan
+from .conceal import DeviceContext, Plan, balance_for_device, build_plan
 from .fse import FseParams
 
 
@@ -48,13 +48,15 @@ def host_group(dist, group=None):
 
 
 def broadcast_plan(mask, params: FseParams, order: str, rank: int, dist, group=None, src: int = 0,
-                   plan_threads: int = 0):
+                   plan_threads: int = 0, precision: str | None = None):
     """Plan the frame on rank `src` only and broadcast the plan's bytes
     (fse_plan_export / fse_plan_import) -- instead of every rank planning the
     same frame with its share of the host CPUs.  `group` must carry CPU
     tensors (gloo), so waiting ranks block in the transport, not on a GPU
     stream.  `plan_threads` is the planning rank's thread count (0 = 3/4 of
-    the usable CPUs: the other ranks are idle meanwhile)."""
+    the usable CPUs: the other ranks are idle meanwhile).  With `precision` the
+    plan's levels are balanced for the planning rank's device before the
+    broadcast (conceal.balance_for_device)."""
     import os
 
     import torch
@@ -62,6 +64,8 @@ def broadcast_plan(mask, params: FseParams, order: str, rank: int, dist, group=N
     if rank == src:
         T = plan_threads or max(1, (3 * len(os.sched_getaffinity(0))) // 4)
         plan = build_plan(mask, params, order, plan_threads=T)
+        if precision is not None:
+            balance_for_device(plan, params, precision)
         data = plan.to_bytes()
         n = torch.tensor([len(data)], dtype=torch.int64)
     else:
@@ -371,9 +375,10 @@ def conceal_strips(image, mask, params: FseParams, precision: str = "fp64", orde
     if world > 1 and plan_on == "rank0":
         hg = host_group(dist, group)
         src = 0 if group is None else dist.get_global_rank(group, 0)
-        plan = broadcast_plan(mask, params, order, rank, dist, hg, src)
+        plan = broadcast_plan(mask, params, order, rank, dist, hg, src, precision=precision)
     else:
         plan = build_plan(mask, params, order)
+        balance_for_device(plan, params, precision)
     B = params.block_size
     R = halo_rows(params)
     processed = (plan.ranks() != np.iinfo(np.int32).max).reshape(plan.rows, plan.cols)

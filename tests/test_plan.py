@@ -433,3 +433,76 @@ def test_band_parallel_planner_edge_grids(shape, B, fill):
         rows = -(-shape[0] // B)
         for T in (2, 3, 7, rows):
             assert _plan_sig(P.build_plan(mask, p, plan_threads=T)) == ref, (T, delta)
+
+
+# ---- level balancing (fse_plan_rebalance): a pure re-leveling
+
+def _check_balanced(plan, lv0, ranks0, batches0, params):
+    lv1 = plan.levels()
+    assert sorted(b for l in lv0 for b in l) == sorted(b for l in lv1 for b in l)
+    assert len(lv1) == len(lv0)
+    np.testing.assert_array_equal(plan.ranks(), ranks0)  # ranks and batches untouched
+    assert plan.batches() == batches0
+    rows, cols = plan.rows, plan.cols
+    level = np.full(rows * cols, -1)
+    for l, bl in enumerate(lv1):
+        level[bl] = l
+    R = -(-params.d // params.block_size)
+    L2, R2 = level.reshape(rows, cols), ranks0.reshape(rows, cols)
+    for r, c in np.argwhere(L2 >= 0):
+        r0, r1, c0, c1 = max(0, r - R), min(rows, r + R + 1), max(0, c - R), min(cols, c + R + 1)
+        dep = (R2[r0:r1, c0:c1] < R2[r, c]) & (L2[r0:r1, c0:c1] >= 0)
+        # every lower-rank block whose samples the window covers runs in an earlier launch
+        assert not dep.any() or L2[r0:r1, c0:c1][dep].max() < L2[r, c], (r, c)
+    return lv1
+
+
+@pytest.mark.parametrize("narrow,wave", [(3, 0), (8, 0), (4, 12), (1, 0)])
+def test_rebalance_keeps_ranks_and_true_dependences(narrow, wave):
+    rng = np.random.default_rng(narrow * 100 + wave)
+    for shape, B, d in [((96, 128), 4, 14), ((70, 90), 8, 9), ((64, 64), 2, 5)]:
+        mask = (rng.uniform(size=(shape[0] // 8 + 1, shape[1] // 8 + 1)) < 0.45).astype(np.uint8)
+        mask = np.kron(mask, np.ones((8, 8), np.uint8))[:shape[0], :shape[1]]
+        p = P.FseParams(d=d, iterations=5, block_size=B, fft_size=64)
+        for order in ("optimized", "linescan"):
+            plan = P.build_plan(mask, p, order)
+            lv0, ranks0, batches0 = plan.levels(), plan.ranks(), plan.batches()
+            moved = plan.rebalance(narrow, wave)
+            lv1 = _check_balanced(plan, lv0, ranks0, batches0, p)
+            assert (moved > 0) == (lv1 != lv0)
+            if wave == 0:  # no level that accepted blocks grew past `narrow`
+                for a, b in zip(lv0, lv1):
+                    assert len(b) <= max(len(a), narrow)
+            # narrow = 0 is a no-op; a second pass finds nothing worse
+            assert plan.rebalance(0, 0) == 0
+            _check_balanced(plan, lv1, ranks0, batches0, p)
+
+
+@pytest.mark.parametrize("i", [0, 1, 2, 4, 8, 9, 10])
+def test_balanced_level_plan_reproduces_reference_on_cpu(golden, i):
+    """The device pipeline emulated on the CPU over BALANCED levels (blocks with
+    slack moved into later, narrower levels) still equals the reference's
+    phase-by-phase result (conceal.py:97-181): only true dependences matter."""
+    c = conceal_case(golden("conceal_cases.npz"), i)
+    plan = P.build_plan(c["mask"], _params(c), c["order"])
+    lv0 = plan.levels()
+    plan.rebalance(2, 0)
+    img, msk = emulate_levels(c["image"], c["mask"], c["block_size"], c["d"], c["rho"], c["delta"],
+                              c["gamma"], c["iterations"], c["fft"], plan.ranks(), plan.levels(),
+                              shuffle_seed=i)
+    np.testing.assert_array_equal(msk, c["out_mask"])
+    assert np.max(np.abs(img - c["out_image"])) <= 1e-9
+    assert sorted(b for l in lv0 for b in l) == sorted(b for l in plan.levels() for b in l)
+
+
+def test_rebalance_survives_export_import_and_rejects_bad_arguments():
+    rng = np.random.default_rng(5)
+    mask = np.kron((rng.uniform(size=(10, 12)) < 0.5).astype(np.uint8), np.ones((8, 8), np.uint8))
+    p = P.FseParams(d=14, iterations=3, block_size=4, fft_size=64)
+    plan = P.build_plan(mask, p)
+    plan.rebalance(5, 0)
+    twin = P.Plan.from_bytes(plan.to_bytes())
+    assert twin.levels() == plan.levels()
+    L = _lib.lib()
+    assert L.fse_plan_rebalance(plan.handle, -1, 0, None) == _lib.FSE_EINVAL
+    assert L.fse_plan_rebalance(None, 1, 0, None) == _lib.FSE_EINVAL
