@@ -121,10 +121,10 @@ int fse_plan_levels(const FsePlan *plan, int32_t *ptr, int32_t *blocks);
  * batches, conceal.py:148-163, stay as they are; this only changes in which
  * LAUNCH a block runs).  Every block sits at its earliest dependency level;
  * blocks with slack (no dependent needs them yet) move from levels wider than
- * `narrow` windows into later levels that still have free slots: up to `narrow`
- * windows in levels that stay at most that wide (the caller passes the SM
- * count: those levels run one window per SM), and, if wave > 0, up to the next
- * multiple of `wave` in wider levels (the resident windows of one wave).
+ * max(narrow, wave) windows into later levels that still have free slots: up
+ * to `narrow` windows in levels that stay at most that wide (the caller passes
+ * the SM count: those levels run one window per SM), and, if wave > 0, up to
+ * `wave` in levels of at most `wave` windows (the resident windows of one wave).
  * Ranks, batches and results are unchanged (only true dependences order the
  * launches).  narrow = 0 leaves the plan as it is.  *moved (optional) = blocks
  * that changed level. */

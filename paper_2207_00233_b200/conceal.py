@@ -124,10 +124,11 @@ def balance_for_device(plan: "Plan", params: FseParams, precision: str, frames: 
     the SM count (levels of at most that many windows run one window per SM, at
     a lone window's latency however few they are, so their free slots take
     blocks of the wide levels for nothing).  Plans of a multi-frame call are
-    left alone: their levels merge across frames.  FSE_BALANCE=0 turns it off;
-    FSE_BALANCE_WAVE=1 selects the variant that only moves the last, partial
-    wave of a wide level (wave = SMs x resident CTAs per SM of the fast kernel),
-    also into levels of less than one wave."""
+    left alone: their levels merge across frames.  Levels of less than one wave
+    (wave = SMs x resident CTAs per SM of the fast kernel) are filled up to the
+    wave as well.  FSE_BALANCE=0 turns it off; FSE_BALANCE_WAVE=0 fills narrow
+    levels only, =2 fills every level of at most one wave up to it (measured in
+    DESIGN.md: 30.8 / 30.4 / 31.8 ms on config 3 for 0 / 1 / 2)."""
     if frames != 1 or os.environ.get("FSE_BALANCE", "1") == "0":
         return 0
     # the pass is sequential (1.3 ms on a 1080p frame at B = 4, 9 ms on a 4K one, 65 ms on a 4K frame at
@@ -145,8 +146,9 @@ def balance_for_device(plan: "Plan", params: FseParams, precision: str, frames: 
     F = params.fft_size if isinstance(params.fft_size, int) else 0
     per_sm = {("fp64", 64): 3, ("fp32", 64): 4, ("fp64", 32): 6, ("fp32", 32): 8,
               ("fp64", 128): 1, ("fp32", 128): 1}.get((precision, F), 0)
-    wave = sms * per_sm if os.environ.get("FSE_BALANCE_WAVE", "0") == "1" else 0
-    return plan.rebalance(sms, wave)
+    mode = os.environ.get("FSE_BALANCE_WAVE", "1")
+    wave = sms * per_sm if mode in ("1", "2") else 0
+    return plan.rebalance(wave if mode == "2" and wave else sms, wave)
 
 
 def _order_code(order: str) -> int:

@@ -971,10 +971,10 @@ void level_csr(Plan &P, const std::vector<int32_t> &level, int n_levels) {
 // never read each other with nonzero weight whatever their ranks (a lower-rank
 // block sees a higher-rank one as lost), so only these true dependences order
 // the launches.  Walking the batches from last to first (every dependent of a
-// block lies in a later batch and is placed before it), a block of the last,
-// partial wave of a level wider than one wave moves to the latest level within
-// its slack that still has free slots: slots up to `narrow` in levels that stay
-// on the one-window-per-SM kernel, up to `wave` in levels of at most one wave.
+// block lies in a later batch and is placed before it), a block of a level wider
+// than max(narrow, wave) moves to the latest level within its slack that still
+// has free slots: slots up to `narrow` in levels that stay on the one-window-
+// per-SM kernel and, with wave > 0, up to `wave` in levels of at most one wave.
 // The slack bound uses the same separable (2R+1)^2 minimum as level_pass's
 // maximum.
 int rebalance_levels(Plan &P, int narrow, int wave) {
@@ -984,21 +984,20 @@ int rebalance_levels(Plan &P, int narrow, int wave) {
     const int R = (P.d + P.B - 1) / P.B;
     const int nb = rows * cols;
     std::vector<int32_t> level(nb, -1);
-    // cap: how many windows a level may hold after accepting blocks; shed: how
-    // many it may give away.  A level wider than one wave gives away only its
-    // last, partial wave (and accepts nothing); a level of at most one wave
-    // accepts up to the wave (or up to `narrow` while it stays that narrow) and
-    // gives nothing away.  Without a wave size (wave = 0) every level wider
-    // than `narrow` may give away any block and only narrow levels accept.
+    // cap: how many windows a level may hold after accepting blocks: `narrow`
+    // while it stays that narrow, `wave` (if given) for a level of at most one
+    // wave; wider levels accept nothing.  shed: how many blocks a level may give
+    // away: any of them, down to `keep` = max(narrow, wave) windows (a level that
+    // accepts gives nothing away).
+    const int keep = std::max(narrow, wave);
     std::vector<int32_t> load(n_levels, 0), cap(n_levels, 0), shed(n_levels, 0);
     for (int l = 0; l < n_levels; ++l) {
         load[l] = P.level_ptr[l + 1] - P.level_ptr[l];
         for (int i = P.level_ptr[l]; i < P.level_ptr[l + 1]; ++i) level[P.level_blocks[i]] = l;
         if (load[l] <= narrow) cap[l] = narrow;
-        else if (wave > 0 && load[l] <= wave) cap[l] = wave;
+        else if (load[l] <= wave) cap[l] = wave;
         else cap[l] = load[l];
-        if (wave > 0) shed[l] = load[l] > wave ? load[l] % wave : 0;
-        else shed[l] = load[l] > narrow ? load[l] : 0;
+        shed[l] = load[l] > keep ? load[l] - keep : 0;
     }
     // latest level <= l with a free slot (union-find over full levels; -1 = none)
     std::vector<int32_t> nf(n_levels + 1);
