@@ -277,8 +277,7 @@ def plan_and_run(masks_host, images_dev, masks_dev, masks_out_dev, params: FsePa
     two: the first chunk (~1/8 of the frames) is planned and its level launches
     queued, then the remaining frames are planned while the GPU works on it.
     Returns the plans (in frame order).  Device work is queued on the current
-    stream (the first chunk on a side stream forked from it and joined before
-    returning); nothing is synchronised."""
+    stream; nothing is synchronised."""
     n = len(masks_host)
     if n == 0:
         return []
@@ -286,40 +285,14 @@ def plan_and_run(masks_host, images_dev, masks_dev, masks_out_dev, params: FsePa
     plans = build_plans(masks_host[:k0], params, order, plan_threads)
     if n == 1:  # one frame: its levels are the launches, balance them (multi-frame levels merge across frames)
         balance_for_device(plans[0], params, precision)
-    side = None
-    if k0 < n and os.environ.get("FSE_OVERLAP_CHUNKS", "1") != "0":
-        # the first chunk runs on a side stream: its narrow last levels (a lone
-        # window's latency each, the GPU nearly empty) then overlap the wide
-        # first levels of the rest, whose frames are independent of it
-        import torch
-
-        cur = torch.cuda.current_stream()
-        DeviceContext.decay(params, max(plans[0].max_wr, plans[0].max_wc, 1))  # created before the fork
-        side = _side_stream()
-        side.wait_stream(cur)
     run_frames_device(plans, images_dev[:k0], masks_dev[:k0],
-                      None if masks_out_dev is None else masks_out_dev[:k0], params, precision,
-                      stream=None if side is None else side.cuda_stream)
+                      None if masks_out_dev is None else masks_out_dev[:k0], params, precision)
     if k0 < n:
         rest = build_plans(masks_host[k0:], params, order, plan_threads)
         run_frames_device(rest, images_dev[k0:], masks_dev[k0:],
                           None if masks_out_dev is None else masks_out_dev[k0:], params, precision)
         plans += rest
-    if side is not None:
-        cur.wait_stream(side)
     return plans
-
-
-_SIDE_STREAMS: dict = {}
-
-
-def _side_stream():
-    import torch
-
-    dev = torch.cuda.current_device()
-    if dev not in _SIDE_STREAMS:
-        _SIDE_STREAMS[dev] = torch.cuda.Stream(device=dev)
-    return _SIDE_STREAMS[dev]
 
 
 def _report(plan: Plan, order, threads, wall) -> ConcealReport:
