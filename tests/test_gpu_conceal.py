@@ -661,3 +661,32 @@ def test_device_entry_points_reject_mismatched_buffers():
         P.run_frames_device([plan], [f64.t()], [m.t()], [out], p, "fp64")
     P.run_frames_device([plan], [f64], [m], [out], p, "fp64")  # the matching call runs
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("prec,B,F", [("fp64", 4, 64), ("fp32", 4, 64), ("fp64", 8, 128), ("fp64", 16, None)])
+def test_level_balancing_never_changes_a_bit(prec, B, F, monkeypatch):
+    """fse_plan_rebalance only changes in which launch a block runs: with it on
+    (the default of one-frame calls) and off, conceal() returns identical bytes,
+    batches (conceal.py:148-163) and picks -- on a frame whose plan really has
+    wide first levels and a narrow tail, so that blocks do move."""
+    from paper_2207_00233_b200 import synth
+
+    img, mask = synth.config_scene(3)
+    img, mask = img[:540, :960].astype(np.float64), mask[:540, :960].copy()
+    img[mask == 1] = 0
+    p = P.FseParams(d=14 if F else 16, iterations=12, block_size=B, fft_size=F)
+    plan = P.build_plan(mask, p)
+    widths = [len(l) for l in plan.levels()]
+    import torch
+
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    moved = plan.rebalance(sms, 0)
+    if F == 64:
+        assert max(widths) > sms and min(widths) < sms and moved > 0
+    monkeypatch.setenv("FSE_BALANCE", "0")
+    off = P.conceal(img, mask, p, precision=prec, return_picks=True)
+    monkeypatch.setenv("FSE_BALANCE", "1")
+    on = P.conceal(img, mask, p, precision=prec, return_picks=True)
+    assert on[0].tobytes() == off[0].tobytes() and on[1].tobytes() == off[1].tobytes()
+    assert on[2].batches == off[2].batches and on[2].blocks_processed == off[2].blocks_processed
+    assert on[3].tobytes() == off[3].tobytes()
