@@ -1016,7 +1016,9 @@ int rebalance_levels(Plan &P, int narrow, int wave) {
     std::vector<int32_t> HM((size_t)rows * cols, kNone);  // min new level of later-batch blocks over row r, columns c +- R
     const int n_batches = (int)P.batch_ptr.size() - 1;
     int moved = 0;
-    for (int k = n_batches - 1; k >= 0; --k) {
+    int64_t free_slots = 0;  // the pass ends when every accepting level is full
+    for (int l = 0; l < n_levels; ++l) free_slots += std::max(0, cap[l] - load[l]);
+    for (int k = n_batches - 1; k >= 0 && free_slots > 0; --k) {
         const int i0 = P.batch_ptr[k], i1 = P.batch_ptr[k + 1];
         for (int i = i0; i < i1; ++i) {
             const int b = P.batch_blocks[i];
@@ -1033,6 +1035,7 @@ int rebalance_levels(Plan &P, int narrow, int wave) {
             --load[lb];
             --shed[lb];
             ++load[t];
+            --free_slots;
             if (full(t)) nf[t + 1] = t;
             level[b] = t;
             ++moved;
