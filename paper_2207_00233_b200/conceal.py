@@ -119,7 +119,7 @@ class Plan:
 _SM_COUNT: dict = {}
 
 
-def balance_for_device(plan: "Plan", params: FseParams, precision: str, frames: int = 1) -> int:
+def balance_for_device(plan: "Plan", params: FseParams, precision: str, frames: int = 1, world: int = 1) -> int:
     """Level balancing of a one-frame plan for the current CUDA device: narrow =
     the SM count (levels of at most that many windows run one window per SM, at
     a lone window's latency however few they are, so their free slots take
@@ -148,6 +148,8 @@ def balance_for_device(plan: "Plan", params: FseParams, precision: str, frames: 
               ("fp64", 128): 1, ("fp32", 128): 1}.get((precision, F), 0)
     mode = os.environ.get("FSE_BALANCE_WAVE", "1")
     wave = sms * per_sm if mode in ("1", "2") else 0
+    # a frame sharded over `world` GPUs (strips) has that many times the slots per level
+    sms, wave = sms * max(1, world), wave * max(1, world)
     return plan.rebalance(wave if mode == "2" and wave else sms, wave)
 
 

@@ -65,7 +65,7 @@ def broadcast_plan(mask, params: FseParams, order: str, rank: int, dist, group=N
         T = plan_threads or max(1, (3 * len(os.sched_getaffinity(0))) // 4)
         plan = build_plan(mask, params, order, plan_threads=T)
         if precision is not None:
-            balance_for_device(plan, params, precision)
+            balance_for_device(plan, params, precision, world=dist.get_world_size(group))
         data = plan.to_bytes()
         n = torch.tensor([len(data)], dtype=torch.int64)
     else:
