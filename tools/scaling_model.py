@@ -90,6 +90,9 @@ def main():
     ap.add_argument("--precision", default="fp32")
     ap.add_argument("--sync-us", type=float, default=4.0,
                     help="per-level neighbour flag wait at N > 1 (cuStreamWaitValue32 + signal kernel)")
+    ap.add_argument("--balance", action="store_true",
+                    help="balance the plan's levels for N GPUs (fse_plan_rebalance with N x the one-GPU capacities)")
+    ap.add_argument("--sms", type=int, default=148)
     a = ap.parse_args()
     cal = load(a.latency, a.precision)
     img, mask = synth.config_scene(5)
@@ -98,19 +101,22 @@ def main():
         if F not in cal:
             continue
         p = P.FseParams(d=14, iterations=100, block_size=B, fft_size=F)
-        plan = P.build_plan(mask, p)
         R = strips.halo_rows(p)
-        rows, cols = plan.rows, plan.cols
-        levels = plan.levels()
-        processed = (plan.ranks() != np.iinfo(np.int32).max).reshape(rows, cols)
-        row_of_level = [np.asarray(lv, np.int64) // cols for lv in levels]
         out, lb, ex = {}, {}, {}
-        lev = np.full(rows * cols, -1, np.int64)
-        for l, blk in enumerate(levels):
-            lev[np.asarray(blk, np.int64)] = l
-        lev = lev.reshape(rows, cols)
-        rank = plan.ranks().astype(np.int64).reshape(rows, cols)
+        per_sm = {("fp64", 64): 3, ("fp32", 64): 4, ("fp64", 32): 6, ("fp32", 32): 8}.get((a.precision, F), 1)
         for N in (1, 2, 4, 8):
+            plan = P.build_plan(mask, p)
+            if a.balance:
+                plan.rebalance(a.sms * N, a.sms * per_sm * N)
+            rows, cols = plan.rows, plan.cols
+            levels = plan.levels()
+            processed = (plan.ranks() != np.iinfo(np.int32).max).reshape(rows, cols)
+            row_of_level = [np.asarray(lv, np.int64) // cols for lv in levels]
+            lev = np.full(rows * cols, -1, np.int64)
+            for l, blk in enumerate(levels):
+                lev[np.asarray(blk, np.int64)] = l
+            lev = lev.reshape(rows, cols)
+            rank = plan.ranks().astype(np.int64).reshape(rows, cols)
             bands = strips.band_partition(processed.sum(axis=1), N, R)
             edges = np.array([b[0] for b in bands] + [bands[-1][1]])
             tot = 0.0
