@@ -150,6 +150,8 @@ def balance_for_device(plan: "Plan", params: FseParams, precision: str, frames: 
     wave = sms * per_sm if mode in ("1", "2") else 0
     # a frame sharded over `world` GPUs (strips) has that many times the slots per level
     sms, wave = sms * max(1, world), wave * max(1, world)
+    if os.environ.get("FSE_BALANCE_NARROW"):  # tests: force moves on small frames
+        sms, wave = int(os.environ["FSE_BALANCE_NARROW"]), 0
     return plan.rebalance(wave if mode == "2" and wave else sms, wave)
 
 
