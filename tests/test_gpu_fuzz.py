@@ -16,10 +16,15 @@ pytest.importorskip("paper_2207_00233_b200")
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
 
 
-@pytest.mark.parametrize("first", [0, 100, 200])
-def test_random_cases_match_the_oracle_up_to_exact_ties(first):
+@pytest.mark.parametrize("first,narrow", [(0, None), (100, None), (200, None), (10000, 2), (10100, 1)])
+def test_random_cases_match_the_oracle_up_to_exact_ties(first, narrow, monkeypatch):
+    """narrow: force the plan's level balancing (fse_plan_rebalance) to move blocks on
+    these small frames -- every level wider than `narrow` windows sheds into later levels."""
     import fuzz_debug
     import fuzz_parity
+
+    if narrow is not None:
+        monkeypatch.setenv("FSE_BALANCE_NARROW", str(narrow))
 
     identical, ties = 0, []
     for seed in range(first, first + 100):
