@@ -6,7 +6,7 @@ the oracle's pick and the device's -- and their relative margin.  A margin at
 rounding level (<~1e-13) is a tie that the DFT's rounding decides (the reference
 computes fft2, the device a separable DFT); a large margin is a device bug.
 
-usage: python tools/fuzz_debug.py seed [seed ...]
+usage: python tests/fuzz_debug.py seed [seed ...]
 """
 import os
 import sys

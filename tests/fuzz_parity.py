@@ -7,7 +7,7 @@ orders, loss patterns from sparse to all lost, rho/delta/gamma, iteration counts
 
 Checked per case: batches, unconcealed blocks and processed count equal, masks
 equal, canonical pick sequences identical for every block, samples within 1e-6.
-A case that differs is examined by tools/fuzz_debug.py: at the first diverging
+A case that differs is examined by tests/fuzz_debug.py: at the first diverging
 pick the two candidates' energies are evaluated in numpy float64 on the oracle's
 own inputs.  Windows with a handful of weighted samples (or a residual already at
 rounding noise) have candidates that agree to ~1e-13 relative or exactly; there
@@ -16,7 +16,7 @@ and the reference's own compiled kernel disagree with each other on about half
 of them), so they are counted as ties, not as device errors.
 The oracle is test infrastructure; this tool only uses it as the checker.
 
-usage: python tools/fuzz_parity.py [n_cases] [first_seed]   (prints one line per case and a summary)
+usage: python tests/fuzz_parity.py [n_cases] [first_seed]   (prints one line per case and a summary)
 """
 import os
 import sys
@@ -121,7 +121,7 @@ if __name__ == "__main__":
                   f"{order} blocks={nb} err={err:.2e}", flush=True)
         except AssertionError as e:
             # a mismatch is a device error unless the first diverging pick is a tie at
-            # rounding level (tools/fuzz_debug.py evaluates the two candidates exactly)
+            # rounding level (tests/fuzz_debug.py evaluates the two candidates exactly)
             from fuzz_debug import debug
 
             print(f"seed {seed}: MISMATCH {e}", flush=True)

@@ -1,8 +1,8 @@
-"""Randomised end-to-end parity (tools/fuzz_parity.py) as a GPU test: 300 seeded
+"""Randomised end-to-end parity (tests/fuzz_parity.py) as a GPU test: 300 seeded
 small frames through conceal() in fp64 against the oracle's restatement of
 fsefill.conceal (conceal.py:97-181) with the reference's kernel
 (_kernel.pyx:128-187).  A case may differ from the oracle only where the first
-diverging pick is a tie at rounding level (tools/fuzz_debug.py evaluates both
+diverging pick is a tie at rounding level (tests/fuzz_debug.py evaluates both
 candidates in float64 on the oracle's inputs); anything else is a device error."""
 
 import os
@@ -13,7 +13,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 pytest.importorskip("paper_2207_00233_b200")
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.parametrize("first,narrow", [(0, None), (100, None), (200, None), (10000, 2), (10100, 1)])
