@@ -155,6 +155,33 @@ def balance_for_device(plan: "Plan", params: FseParams, precision: str, frames: 
     return plan.rebalance(wave if mode == "2" and wave else sms, wave)
 
 
+def balance_batch(plans, params: FseParams, precision: str) -> int:
+    """Level balancing of the plans of one multi-frame session: the session's
+    launches merge each level over the frames of a group (fse_set_groups), so
+    each frame's share of a one-window-per-SM launch is SMs / frames per group.
+    Plans are balanced on host threads (the C call releases the GIL).
+    FSE_BALANCE_BATCH=0 turns it off."""
+    n = len(plans)
+    if n < 2 or os.environ.get("FSE_BALANCE", "1") == "0" or os.environ.get("FSE_BALANCE_BATCH", "1") == "0":
+        return 0
+    import torch
+
+    if not torch.cuda.is_available():
+        return 0
+    dev = torch.cuda.current_device()
+    sms = _SM_COUNT.get(dev)
+    if sms is None:
+        sms = _SM_COUNT[dev] = torch.cuda.get_device_properties(dev).multi_processor_count
+    groups = max(1, min(int(os.environ.get("FSE_GROUPS", "2")), n))
+    narrow = sms * groups // n
+    if narrow < 2:
+        return 0
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=min(n, max(1, (3 * len(os.sched_getaffinity(0))) // 4))) as ex:
+        return sum(ex.map(lambda pl: pl.rebalance(narrow, 0), plans))
+
+
 def _order_code(order: str) -> int:
     return _lib.FSE_ORDER_LINESCAN if order == LINESCAN else _lib.FSE_ORDER_OPTIMIZED
 
@@ -285,14 +312,22 @@ def plan_and_run(masks_host, images_dev, masks_dev, masks_out_dev, params: FsePa
     n = len(masks_host)
     if n == 0:
         return []
-    k0 = n if n < 4 else (first_chunk or max(1, -(-n // 8)))
+    # batches of up to 16 frames run as one session: a first chunk of one or two
+    # frames is a dependency-bound session of its own (config-4 frames, fp64, one
+    # B200: 8 frames 81.6 ms as 1 + 7 vs 70.6 ms as one session, 16 frames 139.2
+    # vs 135.1 ms, 32 frames 266.1 vs 263.3 ms -- there the exposed plan of a
+    # single call costs more than that; FSE_CHUNK_MIN sets the threshold)
+    k0 = n if n < int(os.environ.get("FSE_CHUNK_MIN", "17")) else (first_chunk or max(1, -(-n // 8)))
     plans = build_plans(masks_host[:k0], params, order, plan_threads)
     if n == 1:  # one frame: its levels are the launches, balance them (multi-frame levels merge across frames)
         balance_for_device(plans[0], params, precision)
+    else:
+        balance_batch(plans, params, precision)
     run_frames_device(plans, images_dev[:k0], masks_dev[:k0],
                       None if masks_out_dev is None else masks_out_dev[:k0], params, precision)
     if k0 < n:
         rest = build_plans(masks_host[k0:], params, order, plan_threads)
+        balance_batch(rest, params, precision)
         run_frames_device(rest, images_dev[k0:], masks_dev[k0:],
                           None if masks_out_dev is None else masks_out_dev[k0:], params, precision)
         plans += rest
