@@ -398,7 +398,7 @@ def _chunk_bounds(n: int) -> list:
         fr = [float(x) for x in env.split(",")]
     elif n >= 16:
         fr = [1 / 8, 13 / 16, 1 / 16]
-    elif n >= 4:
+    elif n >= 12:  # (8 frames: 78.3 ms per call as one chunk vs 80.9 ms as 1 + 7)
         fr = [1 / 8, 7 / 8]
     else:
         fr = [1.0]
