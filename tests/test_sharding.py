@@ -79,11 +79,11 @@ def test_conceal_batch_chunk_bounds(monkeypatch):
     """conceal_batch's staged pipeline covers every frame exactly once, in order."""
     from paper_2207_00233_b200.conceal import _chunk_bounds
 
-    for n in (1, 2, 3, 4, 5, 9, 16, 63, 64, 100):
+    for n in (1, 2, 3, 4, 5, 9, 12, 15, 16, 63, 64, 100):
         b = _chunk_bounds(n)
         assert b[0] == 0 and b[-1] == n
         assert all(x < y for x, y in zip(b, b[1:]))
-        assert len(b) == (2 if n < 4 else 3 if n < 16 else 4)
+        assert len(b) == (2 if n < 12 else 3 if n < 16 else 4)
     monkeypatch.setenv("FSE_CHUNKS", "0.0625,0.125,0.6875,0.125")
     for n in (1, 5, 64):
         b = _chunk_bounds(n)
