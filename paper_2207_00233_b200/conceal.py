@@ -525,6 +525,8 @@ def conceal_batch(images, masks, params: FseParams | None = None, order: str = O
         pl = build_plans(list(mh[lo:hi]), params, order, plan_threads)
         if n == 1:
             balance_for_device(pl[0], params, precision)
+        else:
+            balance_batch(pl, params, precision)
         mark(f"plan{c}")
         if c == 1:
             main.wait_event(up)

@@ -28,7 +28,8 @@ import threading
 
 import numpy as np
 
-from .conceal import OPTIMIZED, ORDERS, PRECISIONS, build_plans, run_frames_device
+from .conceal import (OPTIMIZED, ORDERS, PRECISIONS, balance_batch, balance_for_device, build_plans,
+                      run_frames_device)
 from .fse import FseParams
 
 
@@ -110,6 +111,10 @@ class ConcealStream:
                     s["msk_d"][:n].copy_(s["msk_h"][:n], non_blocking=True)
                     up = self._up.record_event()
                 plans = build_plans(list(s["msk_h"][:n].numpy()), self.params, self.order, self.plan_threads)
+                if n == 1:
+                    balance_for_device(plans[0], self.params, self.precision)
+                else:
+                    balance_batch(plans, self.params, self.precision)
                 self._main.wait_event(up)
                 with torch.cuda.stream(self._main):
                     run_frames_device(plans, list(s["img_d"][:n]), list(s["msk_d"][:n]),
