@@ -23,7 +23,8 @@ for batch in (8, 16, 32):
             dt = time.perf_counter() - t
             print(f"stream batch {batch:2d} rep {rep}: {n * loops} frames in {1e3*dt:.1f} ms = {1e3*dt/(n * loops):.2f} ms/frame ({got} back)", flush=True)
 ih = torch.from_numpy(np.stack(imgs)).pin_memory(); mh = torch.from_numpy(np.stack(msks)).pin_memory()
-oi = torch.empty(ih.shape, dtype=torch.float64, pin_memory=True)  # conceal_batch defaults to fp64; om = torch.empty(mh.shape, dtype=torch.uint8, pin_memory=True)
+oi = torch.empty(ih.shape, dtype=torch.float64, pin_memory=True)  # conceal_batch defaults to fp64
+om = torch.empty(mh.shape, dtype=torch.uint8, pin_memory=True)
 for rep in range(3):
     t = time.perf_counter()
     P.conceal_batch(ih, mh, p, out_images=oi, out_masks=om, reports=False)
